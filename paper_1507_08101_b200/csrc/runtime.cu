@@ -1,0 +1,151 @@
+// Per-device runtime: streams, scratch memory, sync policy, error mapping.
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+
+#include "core.cuh"
+
+namespace skb {
+
+const char* errc_name(errc c) {
+    switch (c) {
+        case errc::ok: return "ok";
+        case errc::invalid_arg: return "invalid argument";
+        case errc::overflow: return "index overflow";
+        case errc::shape_mismatch: return "shape mismatch";
+        case errc::pattern_mismatch: return "sparsity pattern mismatch";
+        case errc::io: return "io error";
+        case errc::capacity: return "capacity exceeded";
+        case errc::state: return "invalid state";
+        case errc::alloc: return "allocation failure";
+        case errc::transport: return "transport failure";
+        case errc::unsupported: return "unsupported operation";
+        case errc::numeric: return "numeric failure";
+    }
+    return "unknown";
+}
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    cudaGetLastError();  // clear sticky-free errors
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    if (std::getenv("SELLKIT_VERBOSE")) std::fprintf(stderr, "[sellkit] %s\n", buf);
+    if (e == cudaErrorMemoryAllocation) throw Error(errc::alloc, buf);
+    throw Error(errc::state, buf);
+}
+
+DeviceBuffer::DeviceBuffer(std::size_t bytes, int device) : bytes_(bytes), device_(device) {
+    if (bytes == 0) return;
+    DeviceGuard g(device);
+    CK(cudaMalloc(&ptr_, bytes));
+}
+
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr_) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        if (prev != device_) cudaSetDevice(device_);
+        cudaFree(ptr_);
+        if (prev != device_) cudaSetDevice(prev);
+    }
+}
+
+void* DeviceRuntime::scratch_bytes(std::size_t n) {
+    if (scratch.bytes() < n) {
+        // previous users are stream-ordered on this stream; wait before freeing
+        CK(cudaStreamSynchronize(stream));
+        std::size_t want = std::max<std::size_t>(n, 1 << 20);
+        scratch = DeviceBuffer(want, device);
+    }
+    return scratch.get();
+}
+
+void* DeviceRuntime::pinned_bytes_at_least(std::size_t n) {
+    if (pinned_bytes < n) {
+        CK(cudaStreamSynchronize(stream));
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        std::size_t want = std::max<std::size_t>(n, 4096);
+        CK(cudaMallocHost(&pinned, want));
+        pinned_bytes = want;
+    }
+    return pinned;
+}
+
+namespace {
+std::mutex g_mu;
+std::map<int, DeviceRuntime*>& registry() {
+    static auto* m = new std::map<int, DeviceRuntime*>();  // never destroyed: safe at exit
+    return *m;
+}
+bool g_sync = true;
+}  // namespace
+
+int current_device() {
+    int d = 0;
+    CK(cudaGetDevice(&d));
+    return d;
+}
+
+DeviceRuntime& runtime(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& reg = registry();
+    auto it = reg.find(device);
+    if (it != reg.end()) return *it->second;
+    auto* rt = new DeviceRuntime();
+    rt->device = device;
+    DeviceGuard g(device);
+    CK(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&rt->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int l2 = 0;
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+    rt->l2_bytes = std::size_t(l2);
+    reg[device] = rt;
+    return *rt;
+}
+
+bool sync_mode() { return g_sync; }
+void set_sync_mode(bool s) { g_sync = s; }
+
+void finish(DeviceRuntime& rt) {
+    CK(cudaGetLastError());
+    if (g_sync) CK(cudaStreamSynchronize(rt.stream));
+}
+
+MemKind pointer_kind(const void* p, int* device_out) {
+    cudaPointerAttributes attr{};
+    cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return MemKind::host;
+    }
+    if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+        if (device_out) *device_out = attr.device;
+        return MemKind::device;
+    }
+    return MemKind::host;
+}
+
+namespace {
+// Chunk heights with a dedicated warp-per-32-rows kernel (C divides 32) and
+// block widths with a compile-time-unrolled kernel; see spmv.cu.
+const int kChunkHeights[] = {4, 8, 32};  // == reference config/kernels.cfg:5
+const int kBlockWidths[] = {1, 2, 4, 8, 16, 32, 64};
+}  // namespace
+
+const int* config_chunk_heights(std::size_t* n) {
+    *n = sizeof(kChunkHeights) / sizeof(int);
+    return kChunkHeights;
+}
+const int* config_block_widths(std::size_t* n) {
+    *n = sizeof(kBlockWidths) / sizeof(int);
+    return kBlockWidths;
+}
+lidx row_padding() {
+    lidx p = 1;
+    for (int c : kChunkHeights) p = std::max<lidx>(p, c);
+    return p;
+}
+
+}  // namespace skb

@@ -1,0 +1,402 @@
+// Tall-skinny dense kernels on the device.
+// Reference: /root/reference/proj/src/tsm.hpp:37-305.
+//
+// TSMM      W = alpha*V*X + beta*W : one thread per output element, X (m x k)
+//           staged once per CTA in shared memory, V rows read through L1 (all
+//           lanes of a row share the row's bytes), tmp accumulated over m in the
+//           reference's order.  For m*k <= 64 (HBM-bound shapes) every product
+//           and sum is rounded separately => bit-identical to the reference;
+//           larger shapes are FP64-issue-bound and use FMA (within 1e-12).
+//           beta == 0 => W is not read (BLAS convention; the reference forms
+//           beta*W, which differs only for non-finite W).
+// TSMTTSM   X = alpha*V^H*W + beta*X : each CTA reduces a contiguous row range
+//           (rows staged in shared memory, 32 at a time) into per-thread cell
+//           accumulators, writes its partial m x k block, and an ordered pass
+//           combines CTA partials (Kahan-Babuska-Neumaier on request, like
+//           CompensatedSum tsm.hpp:73-87) and applies alpha/beta.
+#include <algorithm>
+
+#include "ops.cuh"
+#include "tsm.cuh"
+
+namespace skb {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kCellsPerThread = 16;
+constexpr int kRowTile = 32;
+
+__device__ __forceinline__ char* eptr(const DAcc& a, gidx i, gidx j, std::size_t es) {
+    const gidx c = a.cmap ? a.cmap[j] : j;
+    return a.base + ((a.row_offset + i) * a.rs + c * a.cs) * gidx(es);
+}
+template <class T>
+__device__ __forceinline__ T& el(const DAcc& a, gidx i, gidx j) {
+    return *reinterpret_cast<T*>(eptr(a, i, j, sizeof(T)));
+}
+
+template <class T, bool EXACT>
+__device__ __forceinline__ T madd(T acc, T a, T b) {
+    using O = Ops<T>;
+    if constexpr (EXACT) return O::add(acc, O::mul(a, b));
+    else return O::fma(a, b, acc);
+}
+
+// X copied to a dense col-major device array (tsm.hpp:93-98 normalize_small_colmajor)
+template <class T>
+__global__ void x_colmajor_kernel(DAcc x, lidx m, lidx k, T* out) {
+    const gidx t = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
+    if (t >= gidx(m) * k) return;
+    const lidx kk = lidx(t / m), mm = lidx(t % m);
+    out[t] = el<T>(x, mm, kk);
+}
+
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kT) tsmm_kernel(DAcc w, DAcc v, const T* __restrict__ xcm, gidx n, lidx m, lidx k,
+                                                  T alpha, T beta, int beta_zero, int x_in_smem) {
+    using O = Ops<T>;
+    extern __shared__ unsigned char smem_raw[];
+    T* xs = reinterpret_cast<T*>(smem_raw);
+    const T* X = xcm;
+    if (x_in_smem) {
+        for (int t = threadIdx.x; t < m * k; t += blockDim.x) xs[t] = xcm[t];
+        __syncthreads();
+        X = xs;
+    }
+    const gidx total = n * k;
+    for (gidx e = blockIdx.x * gidx(blockDim.x) + threadIdx.x; e < total; e += gidx(gridDim.x) * blockDim.x) {
+        const gidx i = e / k;
+        const lidx kk = lidx(e - i * k);
+        T tmp = O::zero();
+        for (lidx mm = 0; mm < m; ++mm) tmp = madd<T, EXACT>(tmp, el<T>(v, i, mm), X[gidx(kk) * m + mm]);
+        T& wr = el<T>(w, i, kk);
+        wr = beta_zero ? O::mul(alpha, tmp) : O::add(O::mul(alpha, tmp), O::mul(beta, wr));
+    }
+}
+
+// In place: each CTA owns `rows` rows; all outputs are computed into registers
+// before any of them is written back (tsm.hpp:230-249 row-local temp).
+template <class T, bool EXACT>
+__global__ void __launch_bounds__(kT) tsmm_inplace_kernel(DAcc v, const T* __restrict__ xcm, gidx n, lidx m,
+                                                          lidx rows, T alpha, T beta) {
+    using O = Ops<T>;
+    const gidx r0 = gidx(blockIdx.x) * rows;
+    const gidx cnt = min(gidx(rows), n - r0) * m;
+    T out[kCellsPerThread];
+#pragma unroll
+    for (int q = 0; q < kCellsPerThread; ++q) {
+        const gidx e = threadIdx.x + gidx(q) * kT;
+        out[q] = O::zero();
+        if (e < cnt) {
+            const gidx i = r0 + e / m;
+            const lidx kk = lidx(e % m);
+            T s = O::zero();
+            for (lidx mm = 0; mm < m; ++mm) s = madd<T, EXACT>(s, el<T>(v, i, mm), xcm[gidx(kk) * m + mm]);
+            out[q] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kCellsPerThread; ++q) {
+        const gidx e = threadIdx.x + gidx(q) * kT;
+        if (e < cnt) {
+            const gidx i = r0 + e / m;
+            const lidx kk = lidx(e % m);
+            T& vr = el<T>(v, i, kk);
+            vr = O::add(O::mul(alpha, out[q]), O::mul(beta, vr));
+        }
+    }
+}
+
+// Kahan-Babuska-Neumaier step (tsm.hpp:78-85)
+template <class T>
+__device__ __forceinline__ void kbn_add(T& sum, T& comp, T x) {
+    using O = Ops<T>;
+    const T t = O::add(sum, x);
+    if (O::abs2(sum) >= O::abs2(x))
+        comp = O::add(comp, O::add(O::sub(sum, t), x));
+    else
+        comp = O::add(comp, O::add(O::sub(x, t), sum));
+    sum = t;
+}
+
+template <class T, bool KAHAN>
+__global__ void __launch_bounds__(kT) tsmttsm_partial_kernel(DAcc v, DAcc w, gidx n, lidx m, lidx k, gidx rows_per_cta,
+                                                             T* partial, T* pcomp) {
+    using O = Ops<T>;
+    extern __shared__ unsigned char smem_raw[];
+    T* vs = reinterpret_cast<T*>(smem_raw);      // [kRowTile][m]
+    T* ws = vs + kRowTile * m;                   // [kRowTile][k]
+    const gidx cells = gidx(m) * k;
+    const gidx cell0 = gidx(blockIdx.y) * kT * kCellsPerThread;
+    T acc[kCellsPerThread], cmp[kCellsPerThread];
+    lidx cm[kCellsPerThread], ck[kCellsPerThread];
+#pragma unroll
+    for (int q = 0; q < kCellsPerThread; ++q) {
+        acc[q] = O::zero();
+        cmp[q] = O::zero();
+        const gidx c = cell0 + threadIdx.x + gidx(q) * kT;
+        cm[q] = lidx(c % m);  // X accumulators are col-major: cell = kk*m + mm
+        ck[q] = lidx(c / m);
+    }
+    const gidx r_begin = gidx(blockIdx.x) * rows_per_cta;
+    const gidx r_end = min(n, r_begin + rows_per_cta);
+    for (gidx r0 = r_begin; r0 < r_end; r0 += kRowTile) {
+        const int nr = int(min(gidx(kRowTile), r_end - r0));
+        __syncthreads();
+        for (int t = threadIdx.x; t < nr * m; t += kT) vs[t] = O::conj(el<T>(v, r0 + t / m, t % m));
+        for (int t = threadIdx.x; t < nr * k; t += kT) ws[t] = el<T>(w, r0 + t / k, t % k);
+        __syncthreads();
+        for (int r = 0; r < nr; ++r) {
+#pragma unroll
+            for (int q = 0; q < kCellsPerThread; ++q) {
+                if (cell0 + threadIdx.x + gidx(q) * kT < cells) {
+                    const T p = O::mul(vs[r * m + cm[q]], ws[r * k + ck[q]]);
+                    if constexpr (KAHAN) kbn_add(acc[q], cmp[q], p);
+                    else acc[q] = O::add(acc[q], p);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kCellsPerThread; ++q) {
+        const gidx c = cell0 + threadIdx.x + gidx(q) * kT;
+        if (c < cells) {
+            partial[gidx(blockIdx.x) * cells + c] = acc[q];
+            if constexpr (KAHAN) pcomp[gidx(blockIdx.x) * cells + c] = cmp[q];
+        }
+    }
+}
+
+template <class T, bool KAHAN>
+__global__ void tsmttsm_final_kernel(const T* partial, const T* pcomp, int nparts, lidx m, lidx k, DAcc x, T alpha,
+                                     T beta) {
+    using O = Ops<T>;
+    const gidx c = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
+    const gidx cells = gidx(m) * k;
+    if (c >= cells) return;
+    T s = O::zero();
+    if constexpr (KAHAN) {
+        T cs = O::zero();
+        for (int b = 0; b < nparts; ++b) {
+            kbn_add(s, cs, partial[gidx(b) * cells + c]);
+            kbn_add(s, cs, pcomp[gidx(b) * cells + c]);
+        }
+        s = O::add(s, cs);
+    } else {
+        for (int b = 0; b < nparts; ++b) s = O::add(s, partial[gidx(b) * cells + c]);
+    }
+    const lidx mm = lidx(c % m), kk = lidx(c / m);
+    T& xr = el<T>(x, mm, kk);
+    xr = O::add(O::mul(alpha, s), O::mul(beta, xr));
+}
+
+template <class T>
+__global__ void gemm_naive_kernel(DAcc c, DAcc a, DAcc b, lidx n, lidx kc, lidx inner, int ta, int tb, T alpha,
+                                  T beta) {
+    using O = Ops<T>;
+    const gidx t = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
+    if (t >= gidx(n) * kc) return;
+    const lidx i = lidx(t / kc), j = lidx(t % kc);
+    T s = O::zero();
+    for (lidx l = 0; l < inner; ++l) {
+        T av = ta == 0 ? el<T>(a, i, l) : el<T>(a, l, i);
+        if (ta == 2) av = O::conj(av);
+        T bv = tb == 0 ? el<T>(b, l, j) : el<T>(b, j, l);
+        if (tb == 2) bv = O::conj(bv);
+        s = O::add(s, O::mul(av, bv));
+    }
+    T& cr = el<T>(c, i, j);
+    cr = O::add(O::mul(alpha, s), O::mul(beta, cr));
+}
+
+template <class T>
+T scalar_or(const void* p, T dflt) {
+    if (!p) return dflt;
+    T v;
+    std::memcpy(&v, p, sizeof(T));
+    return v;
+}
+
+template <class T>
+bool is_zero(const T& v) {
+    unsigned char z[sizeof(T)] = {};
+    T zero;
+    std::memcpy(&zero, z, sizeof(T));
+    // exact +0 or -0 in every component
+    if constexpr (scalar_traits<T>::is_complex) return v.re == 0 && v.im == 0;
+    else return v == 0;
+}
+
+int grid_cap(gidx work, const DeviceRuntime& rt, int per_sm = 8) {
+    return int(std::max<gidx>(1, std::min<gidx>((work + kT - 1) / kT, gidx(rt.num_sms) * per_sm)));
+}
+
+void check_same_device(const DenseMat& a, const DenseMat& b) {
+    SK_REQUIRE(a.device == b.device, errc::invalid_arg, "operands must live on the same device");
+}
+
+}  // namespace
+
+void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void* alpha, const void* beta, bool kahan) {
+    SK_REQUIRE(v_in.nrows == w_in.nrows, errc::shape_mismatch, "V and W must have equal row counts");
+    SK_REQUIRE(x.nrows == v_in.ncols && x.ncols == w_in.ncols, errc::shape_mismatch, "X must be (V cols) x (W cols)");
+    SK_REQUIRE(x.dt == v_in.dt && x.dt == w_in.dt, errc::invalid_arg, "datatype mismatch between x and v");
+    DenseMat v = v_in, w = w_in;
+    Staged xs(x, true), vs(v, true), wsg(w, true);
+    check_same_device(xs.dev, vs.dev);
+    check_same_device(xs.dev, wsg.dev);
+    const int dev = xs.dev.device;
+    DeviceGuard g(dev);
+    auto& rt = runtime(dev);
+    const lidx m = x.nrows, k = x.ncols;
+    const gidx n = v.nrows;
+    const gidx cells = gidx(m) * k;
+    const int cell_tiles = int((cells + kT * kCellsPerThread - 1) / (kT * kCellsPerThread));
+    const std::size_t es = x.esize();
+    // CTAs over rows: enough to fill the machine, rows per CTA a multiple of the tile
+    const int want = std::max(1, rt.num_sms * 2 / cell_tiles);
+    gidx rows_per = std::max<gidx>(kRowTile, (n + want - 1) / want);
+    rows_per = (rows_per + kRowTile - 1) / kRowTile * kRowTile;
+    const int nparts = int(std::max<gidx>(1, (n + rows_per - 1) / rows_per));
+    const std::size_t smem = std::size_t(kRowTile) * (m + k) * es;
+    SK_REQUIRE(smem <= 200 * 1024, errc::unsupported, "tsmttsm: V/W rows too wide for the staged kernel");
+    auto* part = static_cast<unsigned char*>(rt.scratch_bytes(std::size_t(nparts) * cells * es * 2 + 256));
+    DAcc va = dacc(vs.dev), wa = dacc(wsg.dev), xa = dacc(xs.dev);
+    visit_dt(x.dt, [&]<class T>() {
+        T* p = reinterpret_cast<T*>(part);
+        T* pc = p + std::size_t(nparts) * cells;
+        const T a = scalar_or<T>(alpha, Ops<T>::one()), b = scalar_or<T>(beta, Ops<T>::zero());
+        auto launch = [&](auto kern, auto fin) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            if (n > 0) kern<<<dim3(nparts, cell_tiles), kT, smem, rt.stream>>>(va, wa, n, m, k, rows_per, p, pc);
+            else CK(cudaMemsetAsync(p, 0, std::size_t(nparts) * cells * es * 2, rt.stream));
+            fin<<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, nparts, m, k, xa, a, b);
+        };
+        if (kahan) launch(tsmttsm_partial_kernel<T, true>, tsmttsm_final_kernel<T, true>);
+        else launch(tsmttsm_partial_kernel<T, false>, tsmttsm_final_kernel<T, false>);
+        return 0;
+    });
+    CK(cudaGetLastError());
+    xs.write_back();
+    finish(rt);
+}
+
+void tsmm(DenseMat& w, const DenseMat& v_in, const DenseMat& x_in, const void* alpha, const void* beta) {
+    SK_REQUIRE(w.nrows == v_in.nrows, errc::shape_mismatch, "V and W must have equal row counts");
+    SK_REQUIRE(x_in.nrows == v_in.ncols && x_in.ncols == w.ncols, errc::shape_mismatch, "X must be (V cols) x (W cols)");
+    SK_REQUIRE(w.data != v_in.data, errc::invalid_arg, "V and W must be distinct");
+    SK_REQUIRE(w.dt == v_in.dt && w.dt == x_in.dt, errc::invalid_arg, "datatype mismatch between w and v");
+    DenseMat v = v_in, x = x_in;
+    const lidx m = x.nrows, k = x.ncols;
+    const gidx n = v.nrows;
+    bool beta_zero = false;
+    visit_dt(w.dt, [&]<class T>() {
+        beta_zero = is_zero(scalar_or<T>(beta, Ops<T>::zero()));
+        return 0;
+    });
+    Staged wsg(w, !beta_zero), vs(v, true), xs(x, true);
+    check_same_device(wsg.dev, vs.dev);
+    check_same_device(wsg.dev, xs.dev);
+    const int dev = wsg.dev.device;
+    DeviceGuard g(dev);
+    auto& rt = runtime(dev);
+    const std::size_t es = w.esize();
+    auto* xcm = static_cast<unsigned char*>(rt.scratch_bytes(std::size_t(m) * k * es + 256));
+    DAcc wa = dacc(wsg.dev), va = dacc(vs.dev), xa = dacc(xs.dev);
+    const std::size_t xbytes = std::size_t(m) * k * es;
+    const int x_in_smem = xbytes <= 96 * 1024 ? 1 : 0;
+    const bool exact = gidx(m) * k <= 64;
+    visit_dt(w.dt, [&]<class T>() {
+        T* xc = reinterpret_cast<T*>(xcm);
+        x_colmajor_kernel<T><<<int((gidx(m) * k + 255) / 256), 256, 0, rt.stream>>>(xa, m, k, xc);
+        const T a = scalar_or<T>(alpha, Ops<T>::one()), b = scalar_or<T>(beta, Ops<T>::zero());
+        auto launch = [&](auto kern) {
+            const std::size_t smem = x_in_smem ? xbytes : 0;
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max<std::size_t>(smem, 1))));
+            if (n > 0) kern<<<grid_cap(n * k, rt), kT, smem, rt.stream>>>(wa, va, xc, n, m, k, a, b, beta_zero ? 1 : 0, x_in_smem);
+        };
+        if (exact) launch(tsmm_kernel<T, true>);
+        else launch(tsmm_kernel<T, false>);
+        return 0;
+    });
+    CK(cudaGetLastError());
+    wsg.write_back();
+    finish(rt);
+}
+
+void tsmm_inplace(DenseMat& v, const DenseMat& x_in, const void* alpha, const void* beta) {
+    SK_REQUIRE(x_in.nrows == x_in.ncols, errc::shape_mismatch, "in-place tsmm requires a square X");
+    SK_REQUIRE(x_in.nrows == v.ncols, errc::shape_mismatch, "X must be (V cols) x (V cols)");
+    SK_REQUIRE(v.dt == x_in.dt, errc::invalid_arg, "datatype mismatch between v and x");
+    const lidx m = x_in.nrows;
+    SK_REQUIRE(m <= kT * kCellsPerThread, errc::unsupported, "tsmm_inplace: X wider than 4096 columns");
+    DenseMat x = x_in;
+    Staged vs(v, true), xs(x, true);
+    check_same_device(vs.dev, xs.dev);
+    const int dev = vs.dev.device;
+    DeviceGuard g(dev);
+    auto& rt = runtime(dev);
+    const std::size_t es = v.esize();
+    const gidx n = v.nrows;
+    auto* xcm = static_cast<unsigned char*>(rt.scratch_bytes(std::size_t(m) * m * es + 256));
+    DAcc va = dacc(vs.dev), xa = dacc(xs.dev);
+    const lidx rows = std::max<lidx>(1, (kT * kCellsPerThread) / m);
+    const bool exact = gidx(m) * m <= 64;
+    visit_dt(v.dt, [&]<class T>() {
+        T* xc = reinterpret_cast<T*>(xcm);
+        x_colmajor_kernel<T><<<int((gidx(m) * m + 255) / 256), 256, 0, rt.stream>>>(xa, m, m, xc);
+        const T a = scalar_or<T>(alpha, Ops<T>::one()), b = scalar_or<T>(beta, Ops<T>::zero());
+        const int grid = int((n + rows - 1) / rows);
+        if (grid > 0) {
+            if (exact) tsmm_inplace_kernel<T, true><<<grid, kT, 0, rt.stream>>>(va, xc, n, m, rows, a, b);
+            else tsmm_inplace_kernel<T, false><<<grid, kT, 0, rt.stream>>>(va, xc, n, m, rows, a, b);
+        }
+        return 0;
+    });
+    CK(cudaGetLastError());
+    vs.write_back();
+    finish(rt);
+}
+
+// tsm.hpp:281-305
+void gemm(DenseMat& c, const DenseMat& a_in, const DenseMat& b_in, const void* alpha, const void* beta, Trans ta,
+          Trans tb) {
+    constexpr lidx small = 64;  // small_dim_bound tsm.hpp:13
+    const lidx a_rows = ta == Trans::none ? a_in.nrows : a_in.ncols;
+    const lidx a_cols = ta == Trans::none ? a_in.ncols : a_in.nrows;
+    const lidx b_rows = tb == Trans::none ? b_in.nrows : b_in.ncols;
+    const lidx b_cols = tb == Trans::none ? b_in.ncols : b_in.nrows;
+    SK_REQUIRE(a_cols == b_rows, errc::shape_mismatch, "inner dimensions must agree");
+    SK_REQUIRE(c.nrows == a_rows && c.ncols == b_cols, errc::shape_mismatch, "output shape mismatch");
+    SK_REQUIRE(c.dt == a_in.dt && c.dt == b_in.dt, errc::invalid_arg, "datatype mismatch between c and a");
+    const bool a_tall = a_in.nrows > small && a_in.ncols <= small;
+    const bool conj_ok = !is_complex(c.dt) || ta == Trans::conj_transpose;
+    if (a_tall && ta != Trans::none && conj_ok && tb == Trans::none && b_in.nrows == a_in.nrows && b_in.ncols <= small) {
+        tsmttsm(c, a_in, b_in, alpha, beta, false);
+        return;
+    }
+    if (a_tall && ta == Trans::none && tb == Trans::none && b_in.nrows <= small && b_in.ncols <= small) {
+        tsmm(c, a_in, b_in, alpha, beta);
+        return;
+    }
+    DenseMat a = a_in, b = b_in;
+    Staged cs(c, true), as(a, true), bs(b, true);
+    const int dev = cs.dev.device;
+    DeviceGuard g(dev);
+    auto& rt = runtime(dev);
+    DAcc ca = dacc(cs.dev), aa = dacc(as.dev), ba = dacc(bs.dev);
+    visit_dt(c.dt, [&]<class T>() {
+        const T al = scalar_or<T>(alpha, Ops<T>::one()), be = scalar_or<T>(beta, Ops<T>::zero());
+        const gidx tot = gidx(c.nrows) * c.ncols;
+        gemm_naive_kernel<T><<<int((tot + 255) / 256), 256, 0, rt.stream>>>(ca, aa, ba, c.nrows, c.ncols, a_cols,
+                                                                             int(ta), int(tb), al, be);
+        return 0;
+    });
+    CK(cudaGetLastError());
+    cs.write_back();
+    finish(rt);
+}
+
+}  // namespace skb
