@@ -169,7 +169,13 @@ template <class T, int N>
 __device__ __forceinline__ Vec<T, N> ld_vec(const T* p) {
     Vec<T, N> r;
     constexpr int B = int(sizeof(T)) * N;
-    if constexpr (B == 4 || B == 8 || B == 16) {
+    if constexpr (B == 32) {
+        unsigned long long t[4];
+        asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(t[0]), "=l"(t[1]), "=l"(t[2]), "=l"(t[3])
+                     : "l"(p));
+        memcpy(&r, t, 32);
+    } else if constexpr (B == 4 || B == 8 || B == 16) {
         using R = typename RawVec<B>::type;
         R raw = *reinterpret_cast<const R*>(p);
         memcpy(&r, &raw, B);
@@ -183,7 +189,12 @@ __device__ __forceinline__ Vec<T, N> ld_vec(const T* p) {
 template <class T, int N>
 __device__ __forceinline__ void st_vec(T* p, const Vec<T, N>& v) {
     constexpr int B = int(sizeof(T)) * N;
-    if constexpr (B == 4 || B == 8 || B == 16) {
+    if constexpr (B == 32) {
+        unsigned long long t[4];
+        memcpy(t, &v, 32);
+        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(t[0]), "l"(t[1]), "l"(t[2]), "l"(t[3])
+                     : "memory");
+    } else if constexpr (B == 4 || B == 8 || B == 16) {
         using R = typename RawVec<B>::type;
         R raw;
         memcpy(&raw, &v, B);

@@ -1,0 +1,829 @@
+// SELL-C-sigma SpMV/SpMMV kernel templates for sm_100a (included by the per-type
+// instantiation units spmv_r32.cu / spmv_r64.cu / spmv_c32.cu / spmv_c64.cu and by
+// spmv.cu).  See the comment block below for the design.
+#pragma once
+// SELL-C-sigma SpMV/SpMMV kernels for sm_100a.
+//
+// Reference semantics: /root/reference/proj/src/spmv.hpp:68-92 (generic loop),
+// kernels/spmv_cw.tpl.cpp:10-25 (unrolled C x W variants) and the fused row
+// epilogue spmv_epilogue.hpp:12-36.  Per output element the accumulation order
+// is the reference's (j ascending over the chunk, padding included), and every
+// multiply/add is rounded separately, so y and z are bit-identical to the
+// reference's CPU results.  Dots use a fixed-shape deterministic reduction
+// (warp butterfly -> CTA -> ordered pass over CTAs), equal to the reference
+// within 1e-12 relative (the reference's own dots depend on its worker count).
+//
+// Specialised kernel spmv_cw_kernel<T, C, W>: C in {4, 8, 32} (C divides 32),
+// W in {1, 2, 4, 8, 16, 32, 64}, row-major x/y/z.  One warp owns 32 stored rows
+// (32/C chunks) and a column slice of WS <= 256/sizeof(T) columns:
+//   * lane l streams the value/column of its own row (coalesced 256 B + 128 B
+//     per j for C = 32, L1::no_allocate + L2::evict_first so the RHS block keeps
+//     the caches), and hands them to the TPR lanes that work on that row via
+//     warp shuffles;
+//   * each of the TPR lanes of a row gathers VEC contiguous RHS elements per
+//     load (8/16-byte vector loads through the read-only path), so one warp
+//     instruction reads 32/TPR complete RHS row segments of TPR*VEC*sizeof(T)
+//     contiguous bytes -- the minimal number of L1 wavefronts for a row-major
+//     block vector;
+//   * accumulators: TPR passes x NV vectors x VEC = WS registers-worth per lane.
+// The grid is persistent (occupancy x #SMs CTAs) and warps stride over row
+// groups in ascending order, so all SMs sweep the matrix front-to-back together
+// and the RHS window of a banded/stencil matrix stays L2-resident.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <type_traits>
+
+#include "ops.cuh"
+#include "spmv.cuh"
+#include "tma.cuh"
+
+namespace skb {
+
+template <class T>
+struct KArgs {
+    const gidx* __restrict__ chunk_offset;
+    const lidx* __restrict__ chunk_len;
+    const T* __restrict__ val;
+    const lidx* __restrict__ col;
+    lidx nrows;
+    lidx nrows_padded;
+    gidx nchunks;
+    lidx C;
+    T* y;
+    gidx y_rs, y_cs;
+    const T* x;
+    gidx x_rs, x_cs;
+    const T* xs;  // x of the output row (epilogue); == x except for remote sweeps
+    gidx xs_rs, xs_cs;
+    T* z;
+    gidx z_rs, z_cs;
+    lidx width;
+    std::uint32_t flags;
+    T alpha, beta, gamma, delta, eta;
+    const T* gamma_list;
+    T* partial;
+    const std::uint32_t* defer_mask;
+    const lidx* row_map;
+};
+
+namespace spmv_detail {
+
+constexpr int kBlock = 256;
+constexpr int kWarpsPerBlock = kBlock / 32;
+
+// Work split of a block width over the lanes of a warp (see file comment).
+template <class T, int W, int ACC_BYTES = 256, int VEC_BYTES = 16>
+struct Plan {
+    static constexpr int E = int(sizeof(T));
+    static constexpr int WS_MAX = ACC_BYTES / E;                 // ACC_BYTES/4 32-bit registers of accumulators
+    static constexpr int WS = W < WS_MAX ? W : WS_MAX;           // columns per warp slice
+    static constexpr int NSLICE = W / WS;
+    static constexpr int VEC0 = VEC_BYTES / E;
+    static constexpr int VEC = WS < VEC0 ? WS : VEC0;            // elements per vector load
+    static constexpr int TPR0 = WS / VEC;
+    static constexpr int TPR = TPR0 < 8 ? TPR0 : 8;              // lanes per row
+    static constexpr int NV = WS / (TPR * VEC);                  // vector loads per lane per row
+    static constexpr int RP = 32 / TPR;                          // rows per pass
+    static_assert(W % WS == 0, "width must be a multiple of the slice width");
+    static_assert(kWarpsPerBlock % NSLICE == 0, "slices must tile the CTA");
+};
+
+// j-unroll: as many columns of the chunk in flight as fit ~32 registers of RHS data per lane
+template <class T, class P, int BUDGET = 32>
+constexpr int unroll_of() {
+    constexpr int regs = P::TPR * P::NV * P::VEC * int(sizeof(T)) / 4;
+    constexpr int u = BUDGET / (regs > 0 ? regs : 1);
+    return u < 1 ? 1 : (u > 8 ? 8 : u);
+}
+
+template <class T>
+__device__ __forceinline__ T apply_epilogue(const KArgs<T>& a, T t, T xv, T yv, lidx colidx) {
+    using O = Ops<T>;
+    if (a.flags & kFlagShift) t = O::sub(t, O::mul(a.gamma, xv));
+    if (a.flags & kFlagVshift) t = O::sub(t, O::mul(a.gamma_list[colidx], xv));
+    t = O::mul(t, a.alpha);
+    if (a.flags & kFlagAxpby) t = O::add(t, O::mul(a.beta, yv));
+    return t;
+}
+
+__device__ __forceinline__ bool deferred(const std::uint32_t* mask, gidx row) {
+    return mask && ((mask[row >> 5] >> (row & 31)) & 1u);
+}
+
+template <class T, int C, int W, int U>
+__global__ void __launch_bounds__(kBlock) spmv_cw_kernel(const KArgs<T> a) {
+    using O = Ops<T>;
+    using P = Plan<T, W>;
+    constexpr int VEC = P::VEC, TPR = P::TPR, NV = P::NV, WS = P::WS, NSLICE = P::NSLICE, RP = P::RP;
+    static_assert(32 % C == 0, "chunk height must divide the warp");
+
+    __shared__ T red[kWarpsPerBlock][3][WS];
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const gidx gw = gidx(blockIdx.x) * kWarpsPerBlock + warp;
+    const gidx tw = gidx(gridDim.x) * kWarpsPerBlock;
+    const int slice = int(gw % NSLICE);
+    const int sub = lane % TPR;
+    const int rsub = lane / TPR;
+    const int col_base = slice * WS;
+    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const bool want_dots = (a.flags & kFlagDots) != 0;
+    const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
+    const unsigned long long pol = l2_evict_first_policy();
+
+    T dsum[3][NV][VEC];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) dsum[s][q][e] = O::zero();
+
+    for (gidx rg = gw / NSLICE; rg < ngroups; rg += tw / NSLICE) {
+        const gidx r_own = rg * 32 + lane;
+        const gidx c_own = r_own / C;
+        const lidx i_own = lidx(r_own - c_own * C);
+        gidx off = 0;
+        lidx len = 0;
+        if (c_own < a.nchunks) {
+            off = a.chunk_offset[c_own];
+            len = a.chunk_len[c_own];
+        }
+        const lidx maxlen = (C == 32) ? len : lidx(__reduce_max_sync(0xffffffffu, unsigned(len)));
+        const T* vptr = a.val + off + i_own;
+        const lidx* cptr = a.col + off + i_own;
+
+        T acc[TPR][NV][VEC];
+#pragma unroll
+        for (int p = 0; p < TPR; ++p)
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) acc[p][q][e] = O::zero();
+
+        for (lidx j0 = 0; j0 < maxlen; j0 += U) {
+            T vv[U];
+            lidx cc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const lidx j = j0 + u;
+                if (j < len) {
+                    vv[u] = ld_stream(vptr + gidx(j) * C, pol);
+                    cc[u] = ld_stream(cptr + gidx(j) * C, pol);
+                } else {
+                    vv[u] = O::zero();
+                    cc[u] = -1;
+                }
+            }
+            // branch-free: gather all RHS vectors first (index -1 => row 0, result discarded)
+            T vs[U][TPR];
+            bool ok[U][TPR];
+            Vec<T, VEC> xv[U][TPR][NV];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int p = 0; p < TPR; ++p) {
+                    const int src = p * RP + rsub;
+                    vs[u][p] = (TPR == 1) ? vv[u] : shfl(vv[u], src);
+                    const lidx c = (TPR == 1) ? cc[u] : __shfl_sync(0xffffffffu, cc[u], src);
+                    ok[u][p] = c >= 0;
+                    const T* xr = a.x + gidx(c < 0 ? 0 : c) * a.x_rs + col_base + sub * VEC;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) xv[u][p][q] = ld_x<T, VEC>(xr + q * TPR * VEC);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int p = 0; p < TPR; ++p)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const T s = O::add(acc[p][q][e], O::mul(vs[u][p], xv[u][p][q].v[e]));
+                            acc[p][q][e] = ok[u][p] ? s : acc[p][q][e];
+                        }
+        }
+
+        // fused epilogue (spmv_epilogue.hpp:12-36) for the TPR rows of this lane
+#pragma unroll
+        for (int p = 0; p < TPR; ++p) {
+            const gidx row = rg * 32 + p * RP + rsub;
+            if (row >= a.nrows) continue;
+            const gidx orow = a.row_map ? gidx(a.row_map[row]) : row;
+            const bool fin = !deferred(a.defer_mask, orow);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const int cb = col_base + (q * TPR + sub) * VEC;
+                T* yp = a.y + orow * a.y_rs + cb;
+                Vec<T, VEC> xv, yv, out;
+                if (need_x) xv = ld_x<T, VEC>(a.xs + orow * a.xs_rs + cb);
+                if (a.flags & kFlagAxpby) yv = ld_vec<T, VEC>(yp);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    out.v[e] = apply_epilogue(a, acc[p][q][e], need_x ? xv.v[e] : O::zero(),
+                                              (a.flags & kFlagAxpby) ? yv.v[e] : O::zero(), cb + e);
+                st_vec<T, VEC>(yp, out);
+                if (!fin) continue;
+                if (a.flags & kFlagChain) {
+                    T* zp = a.z + orow * a.z_rs + cb;
+                    Vec<T, VEC> zv = ld_vec<T, VEC>(zp);
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) zv.v[e] = O::add(O::mul(a.delta, zv.v[e]), O::mul(a.eta, out.v[e]));
+                    st_vec<T, VEC>(zp, zv);
+                }
+                if (want_dots) {
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) {
+                        if (a.flags & kFlagDotYY) dsum[0][q][e] = O::add(dsum[0][q][e], O::mul(O::conj(out.v[e]), out.v[e]));
+                        if (a.flags & kFlagDotXY) dsum[1][q][e] = O::add(dsum[1][q][e], O::mul(O::conj(xv.v[e]), out.v[e]));
+                        if (a.flags & kFlagDotXX) dsum[2][q][e] = O::add(dsum[2][q][e], O::mul(O::conj(xv.v[e]), xv.v[e]));
+                    }
+                }
+            }
+        }
+    }
+
+    if (!want_dots) return;  // uniform across the grid
+    // lanes with equal `sub` hold partials of the same columns: butterfly over the row bits
+#pragma unroll
+    for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) dsum[s][q][e] = O::add(dsum[s][q][e], shfl_xor(dsum[s][q][e], m));
+    if (lane < TPR) {
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) red[warp][s][(q * TPR + lane) * VEC + e] = dsum[s][q][e];
+    }
+    __syncthreads();
+    // CTA partial [3][W]: column c belongs to slice c / WS, summed over that slice's warps in order
+    for (int t = threadIdx.x; t < 3 * W; t += kBlock) {
+        const int s = t / W, c = t % W, sl = c / WS, cw = c % WS;
+        T sum = O::zero();
+        for (int w = sl; w < kWarpsPerBlock; w += NSLICE) sum = O::add(sum, red[w][s][cw]);
+        a.partial[gidx(blockIdx.x) * 3 * W + t] = sum;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined variant (the production path for C in {4, 8, 32}).
+//
+// CTA = kNCW consumer warps + 1 producer warp, persistent, tiles of `rgt` row
+// groups (32 rows each) taken in ascending order (tile = blockIdx.x + k*grid).
+// A tile's values and column indices are contiguous in the SELL arrays, so the
+// producer streams each of them with ONE cp.async.bulk into a kStages-deep ring
+// of shared-memory stages (mbarrier transaction counts signal arrival, an
+// "empty" mbarrier per stage returns it).  The matrix stream therefore runs
+// kStages-1 tiles ahead of the math without occupying registers, and the
+// consumers read values/indices with broadcast LDS (no shuffles); only the RHS
+// gathers use LDG (L1-cached, L2-resident window).
+#ifndef SK_NCW
+#define SK_NCW 8
+#endif
+#ifndef SK_STAGE_KB
+#define SK_STAGE_KB 32
+#endif
+#ifndef SK_STAGES
+#define SK_STAGES 3
+#endif
+#ifndef SK_MINB
+#define SK_MINB 2
+#endif
+constexpr int kNCW = SK_NCW;
+constexpr int kTmaThreads = (kNCW + 1) * 32;
+constexpr int kStageBytes = SK_STAGE_KB * 1024;
+constexpr int kStages = SK_STAGES;
+constexpr int kMaxTileChunks = kNCW * 32 / 4;
+
+struct StageHdr {
+    int hoff[kMaxTileChunks + 1];  // slot offset of chunk q relative to the tile start
+    int hlen[kMaxTileChunks];      // chunk lengths
+    int overflow;                  // tile did not fit the stage: read from global
+    int nchunks;
+    long long off0;                // absolute slot offset of the tile
+};
+
+// Work split of the TMA kernel: every consumer warp owns one 32-B column slice of
+// its 32 rows (lane = row, one LDG.256 per nonzero), so the RHS gathers of a warp
+// hit 32 distinct rows and the accumulators stay at 8 registers; wider blocks are
+// split into slices handled by different consumer warps that read the same
+// shared-memory stage (the matrix is fetched from HBM once per tile either way).
+// Measured on B200 (400^3 stencil, w = 8): 1 lane per row beats 2-4 lanes per row.
+#ifndef SK_ACC
+#define SK_ACC 32
+#endif
+#ifndef SK_UBUDGET
+#define SK_UBUDGET 32
+#endif
+template <class T, int W>
+using TPlan = Plan<T, W, (W * int(sizeof(T)) / 8 > SK_ACC ? W * int(sizeof(T)) / 8 : SK_ACC), 32>;
+
+// Stage size: narrow blocks are matrix-stream bound and want deep stages; from
+// 64-B RHS rows on, the RHS gathers dominate and profit from the L1 capacity that
+// smaller stages leave free (measured: w=8 4.7 ms with 32 KB stages, 3.8 ms with 16 KB).
+template <class T, int W>
+struct TmaGeom {
+    static constexpr int SB = (W * int(sizeof(T)) >= 64 ? 16 : kStageBytes / 1024) * 1024;
+    static constexpr int SCAP = (SB / int(sizeof(T) + 4)) / 32 * 32;  // slots per stage
+};
+
+template <class T, int W>
+constexpr std::size_t tma_smem_bytes() {
+    return std::size_t(kStages) * TmaGeom<T, W>::SB + std::size_t(kStages) * sizeof(StageHdr) + 2 * kStages * 8 + 128;
+}
+
+template <class T, int C, int W, int U, bool SMEM>
+__device__ __forceinline__ void tma_rowgroup(const KArgs<T>& a, const T* sval, const lidx* scol, const StageHdr& h,
+                                             int rgi, gidx rg, int slice, int lane,
+                                             T (&acc)[TPlan<T, W>::TPR][TPlan<T, W>::NV][TPlan<T, W>::VEC]) {
+    using O = Ops<T>;
+    using P = TPlan<T, W>;
+    constexpr int VEC = P::VEC, TPR = P::TPR, NV = P::NV, WS = P::WS, RP = P::RP;
+    const int sub = lane % TPR;
+    const int rsub = lane / TPR;
+    const int col_base = slice * WS;
+    // slot of (pass p, j) relative to the stage (or, on overflow, to the tile start):
+    // offp[p] + j*C.  C == 32: one chunk per row group, offp[p] = hoff + row.
+    int offp[TPR];
+    lidx lenp[TPR];
+    lidx maxlen = 0;
+#pragma unroll
+    for (int p = 0; p < TPR; ++p) {
+        const int rp = p * RP + rsub;
+        const int cq = (rgi * 32 + rp) / C;
+        const int ip = (rgi * 32 + rp) % C;
+        lenp[p] = cq < h.nchunks ? h.hlen[cq] : 0;
+        offp[p] = h.hoff[cq] + ip;
+        maxlen = max(maxlen, lenp[p]);
+    }
+    if constexpr (C < 32) maxlen = lidx(__reduce_max_sync(0xffffffffu, unsigned(maxlen)));
+    const T* vbase = SMEM ? sval : a.val + h.off0;
+    const lidx* cbase = SMEM ? scol : a.col + h.off0;
+#pragma unroll
+    for (int p = 0; p < TPR; ++p)
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[p][q][e] = O::zero();
+    lidx minlen = maxlen;
+#pragma unroll
+    for (int p = 0; p < TPR; ++p) minlen = min(minlen, lenp[p]);
+    if constexpr (C < 32) minlen = lidx(__reduce_min_sync(0xffffffffu, unsigned(minlen)));
+    const T* xb = a.x + col_base + sub * VEC;
+    const unsigned xrs = unsigned(a.x_rs);
+
+    // Two-phase body: first every value/index/RHS load of U columns x TPR passes is
+    // issued, then the products are accumulated.  In the main loop every (row, j)
+    // is in range (j < min chunk length of the warp).  In the tail, out-of-range
+    // slots read slot 0 (always present) and the accumulator is kept by a select,
+    // so the result is exactly the reference's (no extra +0 terms).
+    auto body = [&](lidx j0, auto tail) {
+        constexpr bool TAIL = decltype(tail)::value;
+        T vv[U][TPR];
+        Vec<T, VEC> xv[U][TPR][NV];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int p = 0; p < TPR; ++p) {
+                const lidx j = j0 + u;
+                const int slot = (!TAIL || j < lenp[p]) ? offp[p] + j * C : 0;
+                vv[u][p] = vbase[slot];
+                const unsigned c = unsigned(cbase[slot]);
+                const T* xr = xb + std::size_t(c) * xrs;
+#pragma unroll
+                for (int q = 0; q < NV; ++q) xv[u][p][q] = ld_x<T, VEC>(xr + q * TPR * VEC);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int p = 0; p < TPR; ++p) {
+                const bool ok = !TAIL || (j0 + u < lenp[p]);
+#pragma unroll
+                for (int q = 0; q < NV; ++q)
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) {
+                        const T s = O::add(acc[p][q][e], O::mul(vv[u][p], xv[u][p][q].v[e]));
+                        if constexpr (TAIL) acc[p][q][e] = ok ? s : acc[p][q][e];
+                        else acc[p][q][e] = s;
+                    }
+            }
+        }
+    };
+    lidx j0 = 0;
+    for (; j0 + U <= minlen; j0 += U) body(j0, std::false_type{});
+    for (; j0 < maxlen; j0 += U) body(j0, std::true_type{});
+}
+
+template <class T, int C, int W, int U>
+__global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
+    // tile of this CTA's it-th iteration: segments of `seg` consecutive tiles dealt
+    // round-robin over the CTAs (seg = 1: plain round-robin)
+    auto tile_of = [&](int it, int sg) -> gidx {
+        const gidx q = it / sg, w = it % sg;
+        return (q * gridDim.x + blockIdx.x) * sg + w;
+    };
+    using O = Ops<T>;
+    using P = TPlan<T, W>;
+    constexpr int VEC = P::VEC, TPR = P::TPR, NV = P::NV, WS = P::WS, NSLICE = P::NSLICE, RP = P::RP;
+    constexpr int SCAP = TmaGeom<T, W>::SCAP;
+    constexpr int SB = TmaGeom<T, W>::SB;
+    static_assert(32 % C == 0, "chunk height must divide the warp");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ T red[kNCW][3][WS];
+    StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + kStages * SB);
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(hdr + kStages);
+    std::uint64_t* empty = full + kStages;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kNCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int chunks_per_tile = rgt * (32 / C);
+    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const bool want_dots = (a.flags & kFlagDots) != 0;
+
+    if (warp == kNCW) {
+        // ------------------------------------------------------ producer warp
+        const unsigned long long pol = l2_evict_first_policy();
+        for (int it = 0;; ++it) {
+            const gidx t = tile_of(it, seg);
+            if (t >= ntiles) break;
+            const int s = it % kStages;
+            const std::uint32_t k = std::uint32_t(it / kStages);
+            mbar_wait(&empty[s], (k & 1u) ^ 1u);
+            const gidx c0 = t * chunks_per_tile;
+            const gidx c1 = min(a.nchunks, c0 + chunks_per_tile);
+            const int nc = int(c1 - c0);
+            const gidx off0 = a.chunk_offset[c0];
+            for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
+            for (int q = lane; q < nc; q += 32) hdr[s].hlen[q] = a.chunk_len[c0 + q];
+            const gidx nslots = a.chunk_offset[c1] - off0;
+            const bool fits = nslots <= SCAP;
+            if (lane == 0) {
+                hdr[s].overflow = fits ? 0 : 1;
+                hdr[s].nchunks = nc;
+                hdr[s].off0 = off0;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (fits && nslots > 0) {
+                    T* sval = reinterpret_cast<T*>(smem + s * SB);
+                    lidx* scol = reinterpret_cast<lidx*>(smem + s * SB + SCAP * sizeof(T));
+                    const std::uint32_t vb = std::uint32_t(nslots * sizeof(T));
+                    const std::uint32_t cb = std::uint32_t(nslots * sizeof(lidx));
+                    mbar_arrive_expect_tx(&full[s], vb + cb);
+                    bulk_g2s(sval, a.val + off0, vb, &full[s], pol);
+                    bulk_g2s(scol, a.col + off0, cb, &full[s], pol);
+                } else {
+                    mbar_arrive(&full[s]);
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------- consumer warps
+        const int rgi = warp / NSLICE;
+        const int slice = warp % NSLICE;
+        const int sub = lane % TPR;
+        const int rsub = lane / TPR;
+        const int col_base = slice * WS;
+        const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
+        T dsum[3][NV][VEC];
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) dsum[s][q][e] = O::zero();
+        for (int it = 0;; ++it) {
+            const gidx t = tile_of(it, seg);
+            if (t >= ntiles) break;
+            const int s = it % kStages;
+            const std::uint32_t k = std::uint32_t(it / kStages);
+            mbar_wait(&full[s], k & 1u);
+            const gidx rg = t * rgt + rgi;
+            if (rgi < rgt && rg < ngroups) {
+                T acc[TPR][NV][VEC];
+                const T* sval = reinterpret_cast<const T*>(smem + s * SB);
+                const lidx* scol = reinterpret_cast<const lidx*>(smem + s * SB + SCAP * sizeof(T));
+                if (!hdr[s].overflow)
+                    tma_rowgroup<T, C, W, U, true>(a, sval, scol, hdr[s], rgi, rg, slice, lane, acc);
+                else
+                    tma_rowgroup<T, C, W, U, false>(a, sval, scol, hdr[s], rgi, rg, slice, lane, acc);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // matrix data consumed; epilogue touches only x/y/z
+                // fused epilogue (spmv_epilogue.hpp:12-36)
+#pragma unroll
+                for (int p = 0; p < TPR; ++p) {
+                    const gidx row = rg * 32 + p * RP + rsub;
+                    if (row >= a.nrows) continue;
+                    const bool fin = !deferred(a.defer_mask, row);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        const int cb = col_base + (q * TPR + sub) * VEC;
+                        T* yp = a.y + row * a.y_rs + cb;
+                        Vec<T, VEC> xv, yv, out;
+                        if (need_x) xv = ld_x<T, VEC>(a.xs + row * a.xs_rs + cb);
+                        if (a.flags & kFlagAxpby) yv = ld_vec<T, VEC>(yp);
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e)
+                            out.v[e] = apply_epilogue(a, acc[p][q][e], need_x ? xv.v[e] : O::zero(),
+                                                      (a.flags & kFlagAxpby) ? yv.v[e] : O::zero(), cb + e);
+                        st_vec<T, VEC>(yp, out);
+                        if (!fin) continue;
+                        if (a.flags & kFlagChain) {
+                            T* zp = a.z + row * a.z_rs + cb;
+                            Vec<T, VEC> zv = ld_vec<T, VEC>(zp);
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e)
+                                zv.v[e] = O::add(O::mul(a.delta, zv.v[e]), O::mul(a.eta, out.v[e]));
+                            st_vec<T, VEC>(zp, zv);
+                        }
+                        if (want_dots) {
+#pragma unroll
+                            for (int e = 0; e < VEC; ++e) {
+                                if (a.flags & kFlagDotYY)
+                                    dsum[0][q][e] = O::add(dsum[0][q][e], O::mul(O::conj(out.v[e]), out.v[e]));
+                                if (a.flags & kFlagDotXY)
+                                    dsum[1][q][e] = O::add(dsum[1][q][e], O::mul(O::conj(xv.v[e]), out.v[e]));
+                                if (a.flags & kFlagDotXX)
+                                    dsum[2][q][e] = O::add(dsum[2][q][e], O::mul(O::conj(xv.v[e]), xv.v[e]));
+                            }
+                        }
+                    }
+                }
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+        }
+        if (want_dots) {
+#pragma unroll
+            for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) dsum[s][q][e] = O::add(dsum[s][q][e], shfl_xor(dsum[s][q][e], m));
+            if (lane < TPR) {
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) red[warp][s][(q * TPR + lane) * VEC + e] = dsum[s][q][e];
+            }
+        }
+    }
+    if (!want_dots) return;  // uniform across the grid
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * W; t += kTmaThreads) {
+        const int s = t / W, c = t % W, sl = c / WS, cw = c % WS;
+        T sum = O::zero();
+        for (int w = sl; w < kNCW; w += NSLICE) sum = O::add(sum, red[w][s][cw]);
+        a.partial[gidx(blockIdx.x) * 3 * W + t] = sum;
+    }
+}
+
+// Generic fallback (spmv.hpp:68-92): any chunk height, any width, any strides.
+// One thread per (stored row, block of GW columns).
+constexpr int kGW = 8;
+
+template <class T>
+__global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const KArgs<T> a) {
+    using O = Ops<T>;
+    __shared__ T red[3][kGW][kBlock / 32];
+    const int cb0 = blockIdx.y * kGW;
+    const int ncol = min(kGW, a.width - cb0);
+    const bool want_dots = (a.flags & kFlagDots) != 0;
+    const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
+    T dsum[3][kGW];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int e = 0; e < kGW; ++e) dsum[s][e] = O::zero();
+
+    for (gidx r = blockIdx.x * gidx(blockDim.x) + threadIdx.x; r < a.nrows; r += gidx(gridDim.x) * blockDim.x) {
+        const gidx c = r / a.C;
+        const lidx i = lidx(r - c * a.C);
+        const gidx off = a.chunk_offset[c];
+        const lidx cl = a.chunk_len[c];
+        T acc[kGW];
+#pragma unroll
+        for (int e = 0; e < kGW; ++e) acc[e] = O::zero();
+        for (lidx j = 0; j < cl; ++j) {
+            const gidx slot = off + gidx(j) * a.C + i;
+            const T v = a.val[slot];
+            const T* xr = a.x + gidx(a.col[slot]) * a.x_rs + gidx(cb0) * a.x_cs;
+#pragma unroll
+            for (int e = 0; e < kGW; ++e)
+                if (e < ncol) acc[e] = O::add(acc[e], O::mul(v, xr[gidx(e) * a.x_cs]));
+        }
+        const gidx orow = a.row_map ? gidx(a.row_map[r]) : r;
+        const bool fin = !deferred(a.defer_mask, orow);
+#pragma unroll
+        for (int e = 0; e < kGW; ++e) {
+            if (e >= ncol) continue;
+            const int cidx = cb0 + e;
+            T* yp = a.y + orow * a.y_rs + gidx(cidx) * a.y_cs;
+            const T xv = need_x ? a.xs[orow * a.xs_rs + gidx(cidx) * a.xs_cs] : O::zero();
+            const T t = apply_epilogue(a, acc[e], xv, (a.flags & kFlagAxpby) ? *yp : O::zero(), cidx);
+            *yp = t;
+            if (!fin) continue;
+            if (a.flags & kFlagChain) {
+                T* zp = a.z + orow * a.z_rs + gidx(cidx) * a.z_cs;
+                *zp = O::add(O::mul(a.delta, *zp), O::mul(a.eta, t));
+            }
+            if (a.flags & kFlagDotYY) dsum[0][e] = O::add(dsum[0][e], O::mul(O::conj(t), t));
+            if (a.flags & kFlagDotXY) dsum[1][e] = O::add(dsum[1][e], O::mul(O::conj(xv), t));
+            if (a.flags & kFlagDotXX) dsum[2][e] = O::add(dsum[2][e], O::mul(O::conj(xv), xv));
+        }
+    }
+    if (!want_dots) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1)
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int e = 0; e < kGW; ++e) dsum[s][e] = O::add(dsum[s][e], shfl_xor(dsum[s][e], m));
+    if (lane == 0)
+        for (int s = 0; s < 3; ++s)
+            for (int e = 0; e < kGW; ++e) red[s][e][warp] = dsum[s][e];
+    __syncthreads();
+    if (threadIdx.x < 3 * kGW) {
+        const int s = threadIdx.x / kGW, e = threadIdx.x % kGW;
+        T sum = O::zero();
+        for (int w = 0; w < kBlock / 32; ++w) sum = O::add(sum, red[s][e][w]);
+        a.partial[(gidx(blockIdx.y) * gridDim.x + blockIdx.x) * 3 * kGW + threadIdx.x] = sum;
+    }
+}
+
+// Ordered sum over CTA partials.  layout 0: partial[b][3][W]; layout 1:
+// partial[cb][b][3][GW] (generic kernel).  accumulate: out += sum.
+template <class T>
+__global__ void dot_final_kernel(const T* partial, int nparts, int W, int layout, std::uint32_t flags, T* out,
+                                 int accumulate) {
+    using O = Ops<T>;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 3 * W) return;
+    const int s = t / W, c = t % W;
+    if (!(flags & (kFlagDotYY << s))) return;
+    T sum = O::zero();
+    for (int b = 0; b < nparts; ++b) {
+        const gidx idx = layout == 0 ? gidx(b) * 3 * W + t
+                                     : ((gidx(c / kGW) * nparts + b) * 3 + s) * kGW + (c % kGW);
+        sum = O::add(sum, partial[idx]);
+    }
+    out[t] = accumulate ? O::add(out[t], sum) : sum;
+}
+
+// ------------------------------------------------------------------ dispatch
+
+struct LaunchShape {
+    int grid;
+    int nparts;
+    int layout;
+};
+
+template <class K>
+int occupancy_blocks(K kernel) {
+    static std::map<const void*, int> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(reinterpret_cast<const void*>(kernel));
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kBlock, 0));
+    nb = std::max(nb, 1);
+    cache[reinterpret_cast<const void*>(kernel)] = nb;
+    return nb;
+}
+
+// Kernel choice for the specialised shapes: SELLKIT_SPMV_KERNEL = tma | ldg | auto (default auto = tma
+// whenever a row group of the matrix fits one shared-memory stage).
+inline int kernel_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("SELLKIT_SPMV_KERNEL");
+        if (e && std::string(e) == "ldg") return 1;
+        if (e && std::string(e) == "tma") return 2;
+        return 0;
+    }();
+    return mode;
+}
+
+template <class T, int C, int W>
+LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
+    using P = TPlan<T, W>;
+    constexpr int U = unroll_of<T, P, SK_UBUDGET>();
+    auto kern = spmv_tma_kernel<T, C, W, U>;
+    static bool attr = [&] {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tma_smem_bytes<T, W>())));
+        return true;
+    }();
+    (void)attr;
+    static int per_sm = [&] {
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, tma_smem_bytes<T, W>()));
+        return std::max(nb, 1);
+    }();
+    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx ntiles = (ngroups + rgt - 1) / rgt;
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
+    static const int seg = [] {
+        const char* e = std::getenv("SELLKIT_TMA_SEG");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    kern<<<grid, kTmaThreads, tma_smem_bytes<T, W>(), st>>>(a, rgt, ntiles, seg);
+    return {grid, grid, 0};
+}
+
+template <class T, int C, int W>
+LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lidx max_chunk_len) {
+    using P = Plan<T, W>;
+    constexpr int U = unroll_of<T, P>();
+    if (kernel_mode() != 1 && a.row_map == nullptr) {
+        // row groups per tile: as many as fit one stage, at most one per consumer warp (slice)
+        const int cap = TmaGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
+        const int rgt = std::min(kNCW / TPlan<T, W>::NSLICE, cap);
+        if (rgt >= 1) return launch_tma<T, C, W>(a, rgt, rt, st);
+    }
+    auto kern = spmv_cw_kernel<T, C, W, U>;
+    const int per_sm = occupancy_blocks(kern);
+    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx items = ngroups * P::NSLICE;
+    const gidx need = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(need, gidx(per_sm) * rt.num_sms)));
+    kern<<<grid, kBlock, 0, st>>>(a);
+    return {grid, grid, 0};
+}
+
+template <class T>
+LaunchShape launch_generic(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st) {
+    const int ncb = (a.width + kGW - 1) / kGW;
+    const gidx need = (gidx(a.nrows) + kBlock - 1) / kBlock;
+    const int gx = int(std::max<gidx>(1, std::min<gidx>(need, gidx(rt.num_sms) * 8)));
+    spmv_generic_kernel<T><<<dim3(gx, ncb), kBlock, 0, st>>>(a);
+    return {gx, gx, 1};
+}
+
+template <class T, int C>
+bool try_launch_c(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, LaunchShape& ls, lidx mcl) {
+    switch (a.width) {
+        case 1: ls = launch_cw<T, C, 1>(a, rt, st, mcl); return true;
+        case 2: ls = launch_cw<T, C, 2>(a, rt, st, mcl); return true;
+        case 4: ls = launch_cw<T, C, 4>(a, rt, st, mcl); return true;
+        case 8: ls = launch_cw<T, C, 8>(a, rt, st, mcl); return true;
+        case 16: ls = launch_cw<T, C, 16>(a, rt, st, mcl); return true;
+        case 32: ls = launch_cw<T, C, 32>(a, rt, st, mcl); return true;
+        case 64: ls = launch_cw<T, C, 64>(a, rt, st, mcl); return true;
+        default: return false;
+    }
+}
+
+template <class T>
+LaunchShape launch_any(const KArgs<T>& a, bool specialised_ok, DeviceRuntime& rt, cudaStream_t st, lidx mcl) {
+    LaunchShape ls{};
+    if (specialised_ok) {
+        switch (a.C) {
+            case 4:
+                if (try_launch_c<T, 4>(a, rt, st, ls, mcl)) return ls;
+                break;
+            case 8:
+                if (try_launch_c<T, 8>(a, rt, st, ls, mcl)) return ls;
+                break;
+            case 32:
+                if (try_launch_c<T, 32>(a, rt, st, ls, mcl)) return ls;
+                break;
+            default: break;
+        }
+    }
+    return launch_generic<T>(a, rt, st);
+}
+
+}  // namespace spmv_detail
+
+// Launch the best kernel for this shape; explicit instantiations live in spmv_<type>.cu.
+template <class T>
+spmv_detail::LaunchShape launch_spmv(const KArgs<T>& a, bool specialised_ok, DeviceRuntime& rt, cudaStream_t st,
+                                     lidx max_chunk_len);
+
+}  // namespace skb
