@@ -61,6 +61,56 @@ sellkit_error sellkit_ext_densemat_storage(const sellkit_densemat* m, void** dat
  * Row index i is the storage row. */
 sellkit_error sellkit_ext_densemat_fill_hash(sellkit_densemat* m, uint64_t seed);
 
+/* ------------------------------------------ one process per GPU (NCCL) --
+ * The multi-process counterpart of sellkit_ctx (which drives all ranks from one
+ * process).  Each process owns rank `rank` of a BY_ROWS / BY_NNZ partition
+ * (row_offsets[nranks+1], e.g. from sellkit_partition_compute) and passes the
+ * CRS of ITS rows only, with global column indices (sellkit_ext_crs_stencil can
+ * generate such a block on the device).  Setup protocol:
+ *   1. sellkit_ext_rankctx_create             -> local/remote SELL parts on this GPU
+ *   2. for q < recv_count: sellkit_ext_rankctx_recv -> (owner, global columns)
+ *      the caller ships each request to its owner (any transport, e.g.
+ *      torch.distributed); the owner calls sellkit_ext_rankctx_set_sends(to, cols)
+ *   3. rank 0: sellkit_ext_nccl_unique_id; broadcast; all: sellkit_ext_rankctx_connect
+ *   4. sellkit_ext_rank_spmv(y, rc, x, opts, z, nocomm) -- x, y, z hold this rank's
+ *      rows in its stored (sigma-permuted) order (sellkit_ext_rankctx_row_perm).
+ * The halo travels as NCCL send/recv pairs on a communication stream, overlapped
+ * with the local sweep; dots are all-gathered and summed in rank order. */
+typedef struct sellkit_rankctx sellkit_rankctx;
+sellkit_error sellkit_ext_nccl_unique_id(void* id128);
+sellkit_error sellkit_ext_rankctx_create(const sellkit_crs* rows, const sellkit_gidx* row_offsets, int nranks, int rank,
+                                         int chunk_height, int sigma, sellkit_rankctx** out);
+sellkit_error sellkit_ext_rankctx_recv_count(const sellkit_rankctx* rc, int* nowners);
+sellkit_error sellkit_ext_rankctx_recv(const sellkit_rankctx* rc, int q, int* owner, sellkit_lidx* count,
+                                       sellkit_gidx* cols);
+sellkit_error sellkit_ext_rankctx_set_sends(sellkit_rankctx* rc, int to, const sellkit_gidx* cols, sellkit_lidx count);
+sellkit_error sellkit_ext_rankctx_send(const sellkit_rankctx* rc, int s, int* to, sellkit_lidx* count,
+                                       sellkit_lidx* local_rows);
+sellkit_error sellkit_ext_rankctx_connect(sellkit_rankctx* rc, const void* id128);
+sellkit_error sellkit_ext_rank_spmv(sellkit_densemat* y, sellkit_rankctx* rc, const sellkit_densemat* x,
+                                    const sellkit_spmv_opts* opts, sellkit_densemat* z, int nocomm);
+sellkit_error sellkit_ext_rankctx_stats(const sellkit_rankctx* rc, uint64_t* bytes, uint64_t* msgs,
+                                        sellkit_lidx* n_halo, uint64_t* boundary_rows, sellkit_gidx* local_nnz,
+                                        sellkit_gidx* remote_nnz);
+sellkit_error sellkit_ext_rankctx_row_perm(const sellkit_rankctx* rc, sellkit_lidx* row_perm);
+void sellkit_ext_rankctx_destroy(sellkit_rankctx* rc);
+
+/* Host-only planning of one rank (no GPU needed): the partition.hpp:136-220 split
+ * metadata, for tests of the setup protocol on machines without a GPU. */
+typedef struct sellkit_rankplan sellkit_rankplan;
+sellkit_error sellkit_ext_rankplan_create(sellkit_datatype dt, const sellkit_gidx* rowptr, const sellkit_gidx* col,
+                                          const void* val, sellkit_lidx nrows, const sellkit_gidx* row_offsets,
+                                          int nranks, int rank, sellkit_rankplan** out);
+sellkit_error sellkit_ext_rankplan_recv_count(const sellkit_rankplan* rp, int* nowners);
+sellkit_error sellkit_ext_rankplan_recv(const sellkit_rankplan* rp, int q, int* owner, sellkit_lidx* count,
+                                        sellkit_gidx* cols);
+sellkit_error sellkit_ext_rankplan_set_sends(sellkit_rankplan* rp, int to, const sellkit_gidx* cols,
+                                             sellkit_lidx count);
+sellkit_error sellkit_ext_rankplan_nsends(const sellkit_rankplan* rp, int* nsends);
+sellkit_error sellkit_ext_rankplan_send(const sellkit_rankplan* rp, int s, int* to, sellkit_lidx* count,
+                                        sellkit_lidx* local_rows);
+void sellkit_ext_rankplan_destroy(sellkit_rankplan* rp);
+
 #if defined(SELLKIT_BUILD) && defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -14,11 +14,8 @@
 #include <string>
 #include <thread>
 
-#include "dist.cuh"
-#include "objects.cuh"
+#include "handles.cuh"
 #include "ops.cuh"
-#include "sellkit.h"
-#include "sellkit_ext.h"
 #include "spmv.cuh"
 #include "tsm.cuh"
 
@@ -32,57 +29,13 @@ void crs_write_bin(const char* path, const Crs& a, bool wide_cols);
 }  // namespace skb
 
 namespace sk = skb;
-
-struct sellkit_crs {
-    std::unique_ptr<sk::Crs> p;
-};
-struct sellkit_mat {
-    std::unique_ptr<sk::SellMat> p;
-};
-struct sellkit_densemat {
-    sk::DenseMat m;
-};
-struct sellkit_region {
-    std::string name;
-    std::vector<double> samples;
-};
+using sk::dt_from;
+using sk::guarded;
+using sk::order_from;
+using sk::require;
+using sk::same_dt;
 
 namespace {
-
-template <class F>
-sellkit_error guarded(F&& f) noexcept {
-    try {
-        f();
-        return SELLKIT_OK;
-    } catch (const sk::Error& e) {
-        if (std::getenv("SELLKIT_VERBOSE")) std::fprintf(stderr, "[sellkit] %s\n", e.what());
-        return static_cast<sellkit_error>(static_cast<int>(e.code()));
-    } catch (const std::bad_alloc&) {
-        return SELLKIT_ERR_ALLOC;
-    } catch (...) {
-        return SELLKIT_ERR_INVALID_ARG;
-    }
-}
-
-void require(bool cond, const char* msg) {
-    if (!cond) sk::fail(sk::errc::invalid_arg, msg);
-}
-
-sk::Datatype dt_from(sellkit_datatype dt) {
-    switch (dt) {
-        case SELLKIT_R32: return sk::Datatype::r32;
-        case SELLKIT_R64: return sk::Datatype::r64;
-        case SELLKIT_C32: return sk::Datatype::c32;
-        case SELLKIT_C64: return sk::Datatype::c64;
-    }
-    sk::fail(sk::errc::invalid_arg, "unknown datatype");
-}
-
-sk::Order order_from(sellkit_order o) { return o == SELLKIT_ROW_MAJOR ? sk::Order::row_major : sk::Order::col_major; }
-
-void same_dt(sk::Datatype a, sk::Datatype b, const char* what) {
-    if (a != b) sk::fail(sk::errc::invalid_arg, std::string("datatype mismatch between ") + what);
-}
 
 // RowSource -> host CRS (capi.cpp:149-183 / sellcs.hpp:248-265): two passes
 // over the callback (lengths, entries); lengths checked against max_rowlen.

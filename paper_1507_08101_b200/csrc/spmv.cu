@@ -93,6 +93,11 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         a.xs = a.x;
         a.xs_rs = a.x_rs;
         a.xs_cs = a.x_cs;
+        if (hooks.x_self) {
+            a.xs = reinterpret_cast<const T*>(hooks.x_self->data);
+            a.xs_rs = hooks.x_self->row_stride();
+            a.xs_cs = hooks.x_self->col_step();
+        }
         if (o.z) {
             a.z = reinterpret_cast<T*>(o.z->data);
             a.z_rs = o.z->row_stride();

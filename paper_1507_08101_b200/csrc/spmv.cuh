@@ -51,6 +51,7 @@ struct SpmvHooks {
     bool accumulate_dots = false;  // add into `dot_accum` device buffer instead of writing `dot`
     void* dot_accum = nullptr;     // device, 3*width
     cudaStream_t stream = nullptr; // override the runtime stream
+    const DenseMat* x_self = nullptr;  // x of the output rows for shift/dots when x is a halo block
 };
 
 // Validation (spmv.hpp:98-125) + launch.  y/x/z may be host-resident views.

@@ -1,0 +1,336 @@
+"""Host side of the row-distributed SpMMV (reference: proj/src/partition.hpp).
+
+Two entry points over the C ABI:
+
+* :class:`DistContext` -- the reference's single-process API
+  (``sellkit_ctx_create`` / ``sellkit_dvec_*`` / ``sellkit_dist_spmv``): all
+  ranks driven from one process, ranks mapped round-robin onto the visible GPUs.
+* :func:`setup_rank` -- one process per GPU (torchrun).  The C library builds
+  this rank's local/remote SELL parts and moves the halo with NCCL; the only
+  host-side protocol is the exchange of halo requests (each rank tells every
+  owner which of its rows it needs), done here over ``torch.distributed``
+  (gloo or NCCL object collectives) -- :func:`exchange_requests` is also what
+  the CPU (gloo) tests exercise through the host-only ``sellkit_ext_rankplan``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional
+
+import numpy as np
+
+from . import sellkit
+from .sellkit import R64, Sellkit, _ptr, vp
+
+
+def partition(sk: Sellkit, n: int, nranks: int, weights=None, by_nnz: bool = False, rowlens=None) -> np.ndarray:
+    """sellkit_partition_compute (partition.hpp:45-94)."""
+    w = np.ones(nranks) if weights is None else np.ascontiguousarray(weights, np.float64)
+    rl = None if rowlens is None else np.ascontiguousarray(rowlens, np.int32)
+    out = np.zeros(nranks + 1, np.int64)
+    sk.call("sellkit_partition_compute", n, _ptr(rl), _ptr(w), nranks, 1 if by_nnz else 0, _ptr(out))
+    return out
+
+
+# ------------------------------------------------------- single process
+
+class DistContext:
+    """sellkit_ctx: all ranks in this process (reference C ABI, sellkit.h:219-249)."""
+
+    def __init__(self, sk: Sellkit, crs, nranks: int, chunk_height: int, sigma: int, weights=None,
+                 by_nnz: bool = False, record: bool = True):
+        self.sk, self.nranks, self.dt = sk, nranks, crs.dt
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        h = vp()
+        sk.call("sellkit_ctx_create", crs.h, _ptr(w), nranks, 1 if by_nnz else 0, chunk_height, sigma,
+                1 if record else 0, C.byref(h))
+        self.h = h
+
+    def rank_range(self, r):
+        f, c = sellkit.gidx(), sellkit.gidx()
+        self.sk.call("sellkit_ctx_rank_range", self.h, r, C.byref(f), C.byref(c))
+        return f.value, c.value
+
+    def halo_size(self, r):
+        n = sellkit.lidx()
+        self.sk.call("sellkit_ctx_halo_size", self.h, r, C.byref(n))
+        return n.value
+
+    def comm_stats(self):
+        b, m = C.c_uint64(), C.c_uint64()
+        self.sk.call("sellkit_ctx_comm_stats", self.h, C.byref(b), C.byref(m))
+        return b.value, m.value
+
+    def reset_comm_stats(self):
+        self.sk.call("sellkit_ctx_reset_comm_stats", self.h)
+
+    def vec(self, width: int, order=sellkit.ROW_MAJOR) -> "DistVec":
+        h = vp()
+        self.sk.call("sellkit_dvec_create", self.h, width, order, C.byref(h))
+        return DistVec(self, h, width)
+
+    def scatter(self, global_mat, v: "DistVec"):
+        self.sk.call("sellkit_dvec_scatter", self.h, global_mat.h, v.h)
+
+    def gather(self, v: "DistVec", out):
+        self.sk.call("sellkit_dvec_gather", self.h, v.h, out.h)
+
+    def spmv(self, y: "DistVec", x: "DistVec", flags=0, alpha=None, beta=None, gamma=None, delta=None, eta=None,
+             z: Optional["DistVec"] = None, dot: Optional[np.ndarray] = None, mode=sellkit.NO_OVERLAP,
+             nocomm: bool = False):
+        o = sellkit.spmv_opts()
+        keep = []
+
+        def sc(v):
+            if v is None:
+                return None
+            a = np.ascontiguousarray(np.atleast_1d(v), dtype=sellkit.NP_DTYPE[self.dt])
+            keep.append(a)
+            return _ptr(a)
+        o.flags = flags
+        o.alpha, o.beta, o.gamma, o.delta, o.eta = sc(alpha), sc(beta), sc(gamma), sc(delta), sc(eta)
+        o.dot = _ptr(dot)
+        if nocomm:
+            self.sk.call("sellkit_spmv_nocomm", y.h, self.h, x.h, C.byref(o), z.h if z is not None else None)
+        else:
+            self.sk.call("sellkit_dist_spmv", y.h, self.h, x.h, C.byref(o), mode, z.h if z is not None else None, 4)
+
+    def close(self):
+        if self.h:
+            self.sk.lib.sellkit_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DistVec:
+    def __init__(self, ctx: DistContext, h, width):
+        self.ctx, self.h, self.width = ctx, h, width
+
+    def close(self):
+        if self.h:
+            self.ctx.sk.lib.sellkit_dvec_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------- one process per GPU
+
+def exchange_requests(my_requests: Dict[int, np.ndarray], rank: int, world: int, group=None) -> Dict[int, np.ndarray]:
+    """All-to-all of halo requests: returns {requester: global columns it needs from `rank`}."""
+    import torch.distributed as tdist
+    gathered: List[Optional[Dict[int, np.ndarray]]] = [None] * world
+    tdist.all_gather_object(gathered, {int(k): np.asarray(v, np.int64) for k, v in my_requests.items()}, group=group)
+    return {r: gathered[r][rank] for r in range(world) if r != rank and rank in gathered[r]}
+
+
+def _requests(sk: Sellkit, h, prefix: str) -> Dict[int, np.ndarray]:
+    n = C.c_int()
+    sk.call(f"sellkit_ext_{prefix}_recv_count", h, C.byref(n))
+    out = {}
+    for q in range(n.value):
+        owner, cnt = C.c_int(), sellkit.lidx()
+        sk.call(f"sellkit_ext_{prefix}_recv", h, q, C.byref(owner), C.byref(cnt), None)
+        cols = np.zeros(cnt.value, np.int64)
+        sk.call(f"sellkit_ext_{prefix}_recv", h, q, None, None, _ptr(cols))
+        out[owner.value] = cols
+    return out
+
+
+class RankPlan:
+    """Host-only plan of one rank (sellkit_ext_rankplan_*; no GPU needed)."""
+
+    def __init__(self, sk: Sellkit, rowptr, col, val, row_offsets, rank: int, dt=R64):
+        self.sk = sk
+        self._keep = [np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int64),
+                      np.ascontiguousarray(val, sellkit.NP_DTYPE[dt]), np.ascontiguousarray(row_offsets, np.int64)]
+        rp, cl, vl, off = self._keep
+        h = vp()
+        sk.call("sellkit_ext_rankplan_create", dt, _ptr(rp), _ptr(cl), _ptr(vl), len(rp) - 1, _ptr(off),
+                len(off) - 1, rank, C.byref(h))
+        self.h = h
+
+    def requests(self) -> Dict[int, np.ndarray]:
+        return _requests(self.sk, self.h, "rankplan")
+
+    def set_sends(self, to: int, cols: np.ndarray):
+        cols = np.ascontiguousarray(cols, np.int64)
+        self.sk.call("sellkit_ext_rankplan_set_sends", self.h, to, _ptr(cols), len(cols))
+
+    def sends(self) -> Dict[int, np.ndarray]:
+        n = C.c_int()
+        self.sk.call("sellkit_ext_rankplan_nsends", self.h, C.byref(n))
+        out = {}
+        for s in range(n.value):
+            to, cnt = C.c_int(), sellkit.lidx()
+            self.sk.call("sellkit_ext_rankplan_send", self.h, s, C.byref(to), C.byref(cnt), None)
+            rows = np.zeros(cnt.value, np.int32)
+            self.sk.call("sellkit_ext_rankplan_send", self.h, s, None, None, _ptr(rows))
+            out[to.value] = rows
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.sk.lib.sellkit_ext_rankplan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class RankContext:
+    """sellkit_ext_rankctx: this process's rank of a distributed matrix."""
+
+    def __init__(self, sk: Sellkit, rows_crs, row_offsets, rank: int, chunk_height: int, sigma: int):
+        self.sk = sk
+        self.row_offsets = np.ascontiguousarray(row_offsets, np.int64)
+        self.rank, self.world = rank, len(self.row_offsets) - 1
+        self.dt = rows_crs.dt
+        self.nrows = int(self.row_offsets[rank + 1] - self.row_offsets[rank])
+        h = vp()
+        sk.call("sellkit_ext_rankctx_create", rows_crs.h, _ptr(self.row_offsets), self.world, rank, chunk_height,
+                sigma, C.byref(h))
+        self.h = h
+
+    def requests(self) -> Dict[int, np.ndarray]:
+        return _requests(self.sk, self.h, "rankctx")
+
+    def set_sends(self, to: int, cols: np.ndarray):
+        cols = np.ascontiguousarray(cols, np.int64)
+        self.sk.call("sellkit_ext_rankctx_set_sends", self.h, to, _ptr(cols), len(cols))
+
+    def connect(self, nccl_id: bytes):
+        buf = (C.c_char * 128).from_buffer_copy(nccl_id)
+        self.sk.call("sellkit_ext_rankctx_connect", self.h, C.cast(buf, vp))
+
+    def row_perm(self) -> np.ndarray:
+        out = np.zeros(self.nrows, np.int32)
+        self.sk.call("sellkit_ext_rankctx_row_perm", self.h, _ptr(out))
+        return out
+
+    def stats(self):
+        b, m, nh, br, ln, rn = (C.c_uint64(), C.c_uint64(), sellkit.lidx(), C.c_uint64(), sellkit.gidx(),
+                                sellkit.gidx())
+        self.sk.call("sellkit_ext_rankctx_stats", self.h, C.byref(b), C.byref(m), C.byref(nh), C.byref(br),
+                     C.byref(ln), C.byref(rn))
+        return dict(bytes=b.value, msgs=m.value, n_halo=nh.value, boundary_rows=br.value, local_nnz=ln.value,
+                    remote_nnz=rn.value)
+
+    def spmv(self, y, x, flags=0, alpha=None, beta=None, gamma=None, delta=None, eta=None, z=None,
+             dot: Optional[np.ndarray] = None, nocomm: bool = False, opts=None):
+        if opts is None:
+            opts = sellkit.spmv_opts()
+            keep = []
+
+            def sc(v):
+                if v is None:
+                    return None
+                a = np.ascontiguousarray(np.atleast_1d(v), dtype=sellkit.NP_DTYPE[self.dt])
+                keep.append(a)
+                return _ptr(a)
+            opts.flags = flags
+            opts.alpha, opts.beta, opts.gamma, opts.delta, opts.eta = sc(alpha), sc(beta), sc(gamma), sc(delta), sc(eta)
+            opts.dot = _ptr(dot)
+        self.sk.call("sellkit_ext_rank_spmv", y.h, self.h, x.h, C.byref(opts), z.h if z is not None else None,
+                     1 if nocomm else 0)
+
+    def close(self):
+        if self.h:
+            self.sk.lib.sellkit_ext_rankctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def setup_rank(sk: Sellkit, rows_crs, row_offsets, rank: int, world: int, chunk_height: int, sigma: int,
+               group=None) -> RankContext:
+    """Build this rank's parts, exchange halo requests, connect NCCL."""
+    import torch.distributed as tdist
+    rc = RankContext(sk, rows_crs, row_offsets, rank, chunk_height, sigma)
+    if world > 1:
+        incoming = exchange_requests(rc.requests(), rank, world, group)
+        for to in sorted(incoming):
+            rc.set_sends(to, incoming[to])
+        idbuf = bytearray(128)
+        if rank == 0:
+            raw = (C.c_char * 128)()
+            sk.call("sellkit_ext_nccl_unique_id", C.cast(raw, vp))
+            idbuf = bytearray(raw.raw)
+        obj = [bytes(idbuf)]
+        tdist.broadcast_object_list(obj, src=0, group=group)
+        rc.connect(obj[0])
+    else:
+        rc.connect(bytes(128))
+    return rc
+
+
+# ------------------------------------------------------------------ bench
+
+@dataclass
+class BenchJob:
+    step: Callable[[], None]
+    e2e_step: Callable[[], None]
+    rows_local: int
+    nnz_local: int
+    halo_bytes: int
+    launches_per_step: int
+    h2d_bytes: int
+    d2h_bytes: int
+    keep: list = field(default_factory=list)
+
+    def kernel_ms(self, per_step: List[float]) -> float:
+        return float(np.mean(per_step))
+
+
+def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank: int, world: int) -> BenchJob:
+    """This rank's z-slab of the n^3 7-point stencil (BY_ROWS, equal weights), x hashed on the device."""
+    import torch
+    N = n ** 3
+    off = partition(sk, N, world)
+    r0, r1 = int(off[rank]), int(off[rank + 1])
+    rows = sk.crs_stencil(7, n, r0, r1)
+    _, _, nnz_local = rows.dims()
+    rc = setup_rank(sk, rows, off, rank, world, chunk_height, sigma)
+    del rows
+    nloc = r1 - r0
+    x = sk.densemat(nloc, w)
+    x.fill_hash(42 + rank)
+    y = sk.densemat(nloc, w)
+    st = rc.stats()
+    opts = sellkit.spmv_opts()
+    sk.lib.sellkit_spmv_opts_init(C.byref(opts))
+
+    def step():
+        sk.call("sellkit_ext_rank_spmv", y.h, rc.h, x.h, C.byref(opts), None, 0)
+
+    xh = torch.empty((nloc, w), dtype=torch.float64, pin_memory=True)
+    yh = torch.empty((nloc, w), dtype=torch.float64, pin_memory=True)
+    sk.call("sellkit_densemat_copy_out", x.h, vp(xh.data_ptr()), nloc * w)
+
+    def e2e_step():
+        sk.call("sellkit_densemat_copy_in", x.h, vp(xh.data_ptr()), nloc * w)
+        step()
+        sk.call("sellkit_densemat_copy_out", y.h, vp(yh.data_ptr()), nloc * w)
+
+    # our kernels per step: pack (one per send list) + local sweep + remote sweep; the stencil
+    # coupling is symmetric, so we send to exactly the owners we receive from
+    nsend = len(rc.requests())
+    launches = 1 + (1 + nsend if world > 1 and st["boundary_rows"] > 0 else 0)
+    halo_bytes = st["n_halo"] * w * 8
+    return BenchJob(step=step, e2e_step=e2e_step, rows_local=nloc, nnz_local=nnz_local, halo_bytes=halo_bytes,
+                    launches_per_step=launches, h2d_bytes=nloc * w * 8, d2h_bytes=nloc * w * 8,
+                    keep=[rc, x, y, xh, yh, opts])

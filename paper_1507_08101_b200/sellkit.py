@@ -154,6 +154,25 @@ _EXT = [
     ("sellkit_ext_densemat_storage", err_t, [vp, C.POINTER(vp), C.POINTER(lidx), C.POINTER(C.c_int),
                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("sellkit_ext_densemat_fill_hash", err_t, [vp, C.c_uint64]),
+    ("sellkit_ext_nccl_unique_id", err_t, [vp]),
+    ("sellkit_ext_rankctx_create", err_t, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    ("sellkit_ext_rankctx_recv_count", err_t, [vp, C.POINTER(C.c_int)]),
+    ("sellkit_ext_rankctx_recv", err_t, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(lidx), vp]),
+    ("sellkit_ext_rankctx_set_sends", err_t, [vp, C.c_int, vp, lidx]),
+    ("sellkit_ext_rankctx_send", err_t, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(lidx), vp]),
+    ("sellkit_ext_rankctx_connect", err_t, [vp, vp]),
+    ("sellkit_ext_rank_spmv", err_t, [vp, vp, vp, C.POINTER(spmv_opts), vp, C.c_int]),
+    ("sellkit_ext_rankctx_stats", err_t, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(lidx),
+                                          C.POINTER(C.c_uint64), C.POINTER(gidx), C.POINTER(gidx)]),
+    ("sellkit_ext_rankctx_row_perm", err_t, [vp, vp]),
+    ("sellkit_ext_rankctx_destroy", None, [vp]),
+    ("sellkit_ext_rankplan_create", err_t, [C.c_int, vp, vp, vp, lidx, vp, C.c_int, C.c_int, C.POINTER(vp)]),
+    ("sellkit_ext_rankplan_recv_count", err_t, [vp, C.POINTER(C.c_int)]),
+    ("sellkit_ext_rankplan_recv", err_t, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(lidx), vp]),
+    ("sellkit_ext_rankplan_set_sends", err_t, [vp, C.c_int, vp, lidx]),
+    ("sellkit_ext_rankplan_nsends", err_t, [vp, C.POINTER(C.c_int)]),
+    ("sellkit_ext_rankplan_send", err_t, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(lidx), vp]),
+    ("sellkit_ext_rankplan_destroy", None, [vp]),
 ]
 
 API_NAMES = [n for n, _, _ in _API]
