@@ -178,6 +178,11 @@ struct DeviceRuntime {
     void* pinned = nullptr;  // small pinned staging area for dot results
     std::size_t pinned_bytes = 0;
     std::mutex mu;
+    // copy streams + device staging of the streamed host-buffer spmv (spmv.cu)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    DeviceBuffer stage[3];
+    void* stage_bytes(int i, std::size_t n);
+    void copy_streams();
 
     void* scratch_bytes(std::size_t n);
     void* pinned_bytes_at_least(std::size_t n);

@@ -49,6 +49,9 @@ struct SellMat {
     DeviceBuffer row_perm;      // int32 [nrows]   original -> stored
     DeviceBuffer row_perm_inv;  // int32 [nrows]   stored -> original
     DeviceBuffer rowlen;        // int32 [nrows_padded]
+    // streamed host-buffer spmv: largest column index per row-group block (lazily computed)
+    mutable std::vector<lidx> watermark;
+    mutable int watermark_blocks = 0;
 };
 
 struct BuildOptions {

@@ -61,6 +61,23 @@ void* DeviceRuntime::scratch_bytes(std::size_t n) {
     return scratch.get();
 }
 
+void* DeviceRuntime::stage_bytes(int i, std::size_t n) {
+    if (stage[i].bytes() < n) {
+        CK(cudaDeviceSynchronize());
+        stage[i] = DeviceBuffer();
+        stage[i] = DeviceBuffer(n, device);
+    }
+    return stage[i].get();
+}
+
+void DeviceRuntime::copy_streams() {
+    if (!h2d) {
+        DeviceGuard g(device);
+        CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    }
+}
+
 void* DeviceRuntime::pinned_bytes_at_least(std::size_t n) {
     if (pinned_bytes < n) {
         CK(cudaStreamSynchronize(stream));

@@ -15,7 +15,6 @@ T scalar_of(const unsigned char* b) {
     return v;
 }
 
-// 16-B aligned view: every vector access of the specialised kernel is legal.
 // Every row segment a specialised kernel touches with one vector access must be
 // aligned to the access width: min(32 B, width * element bytes) (widths are powers of 2).
 bool aligned_for_vectors(const DenseMat& m) {
@@ -24,7 +23,153 @@ bool aligned_for_vectors(const DenseMat& m) {
     return (reinterpret_cast<std::uintptr_t>(m.data) % req == 0) && ((std::size_t(m.stride) * m.esize()) % req == 0);
 }
 
+// largest column index of each block of row groups [rgb[b], rgb[b+1])
+__global__ void watermark_kernel(const lidx* col, const gidx* chunk_offset, const gidx* cbeg, int nb, lidx* out) {
+    const int b = blockIdx.y;
+    if (b >= nb) return;
+    const gidx s0 = chunk_offset[cbeg[b]], s1 = chunk_offset[cbeg[b + 1]];
+    lidx m = 0;
+    for (gidx s = s0 + blockIdx.x * gidx(blockDim.x) + threadIdx.x; s < s1; s += gidx(gridDim.x) * blockDim.x)
+        m = max(m, col[s]);
+    m = lidx(__reduce_max_sync(0xffffffffu, unsigned(m)));
+    if ((threadIdx.x & 31) == 0) atomicMax(&out[b], m);
+}
+
+bool pinned_host(const DenseMat& m) {
+    if (m.mem != MemKind::host || m.scattered() || m.order != Order::row_major || m.stride != m.ncols) return false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, m.data) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
 }  // namespace
+
+// Streamed spmv on pinned host buffers: x arrives in row slabs on one copy engine,
+// each block of row groups is swept as soon as the x rows up to its largest column
+// index are resident (column watermark), and its y rows leave on the other copy
+// engine -- H2D, sweep and D2H overlap instead of running back to back.
+static bool spmv_host_streamed(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& o) {
+    const bool chain = (o.flags & kFlagChain) != 0;
+    const bool ok = pinned_host(x) && pinned_host(y) && (!chain || pinned_host(*o.z));
+    if (std::getenv("SELLKIT_VERBOSE"))
+        std::fprintf(stderr, "[sellkit] host-buffer spmv: %s\n", ok ? "streamed" : "staged (buffers not pinned)");
+    if (!ok) return false;
+    auto& rt = runtime(A.device);
+    rt.copy_streams();
+    const gidx ngroups = (gidx(A.nrows_padded) + 31) / 32;
+    const int nb = int(std::min<gidx>(16, ngroups));
+    if (nb < 2) return false;
+    const std::size_t es = value_bytes(A.dt);
+    const lidx w = x.ncols;
+    const std::size_t xrow = std::size_t(w) * es;
+    std::vector<gidx> rgb(std::size_t(nb) + 1);
+    for (int b = 0; b <= nb; ++b) rgb[b] = ngroups * b / nb;
+    if (A.watermark_blocks != nb) {
+        const int cpr = A.C >= 32 ? 1 : 32 / A.C;  // chunks per row group (C divides 32 or C >= 32)
+        std::vector<gidx> cbeg(std::size_t(nb) + 1);
+        for (int b = 0; b <= nb; ++b)
+            cbeg[b] = A.C <= 32 && 32 % A.C == 0 ? std::min<gidx>(A.nchunks, rgb[b] * cpr)
+                                                 : std::min<gidx>(A.nchunks, (rgb[b] * 32 + A.C - 1) / A.C);
+        DeviceBuffer d_cb(cbeg.size() * sizeof(gidx), A.device), d_wm(std::size_t(nb) * sizeof(lidx), A.device);
+        CK(cudaMemcpyAsync(d_cb.get(), cbeg.data(), cbeg.size() * sizeof(gidx), cudaMemcpyHostToDevice, rt.stream));
+        CK(cudaMemsetAsync(d_wm.get(), 0, std::size_t(nb) * sizeof(lidx), rt.stream));
+        watermark_kernel<<<dim3(64, nb), 256, 0, rt.stream>>>(A.col.as<lidx>(), A.chunk_offset.as<gidx>(),
+                                                             d_cb.as<gidx>(), nb, d_wm.as<lidx>());
+        CK(cudaGetLastError());
+        A.watermark.assign(std::size_t(nb), 0);
+        CK(cudaMemcpyAsync(A.watermark.data(), d_wm.get(), std::size_t(nb) * sizeof(lidx), cudaMemcpyDeviceToHost,
+                           rt.stream));
+        CK(cudaStreamSynchronize(rt.stream));
+        A.watermark_blocks = nb;
+    }
+    auto* xd = static_cast<unsigned char*>(rt.stage_bytes(0, std::size_t(x.nrows) * xrow));
+    auto* yd = static_cast<unsigned char*>(rt.stage_bytes(1, std::size_t(y.nrows) * xrow));
+    unsigned char* zd = chain ? static_cast<unsigned char*>(rt.stage_bytes(2, std::size_t(y.nrows) * xrow)) : nullptr;
+    DenseMat xdev = densemat_view_plain(A.dt, xd, std::size_t(x.nrows) * w, x.nrows, w, w, Order::row_major);
+    DenseMat ydev = densemat_view_plain(A.dt, yd, std::size_t(y.nrows) * w, y.nrows, w, w, Order::row_major);
+    DenseMat zdev;
+    if (chain) zdev = densemat_view_plain(A.dt, zd, std::size_t(y.nrows) * w, y.nrows, w, w, Order::row_major);
+
+    std::vector<cudaEvent_t> ev(3 * std::size_t(nb));
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* ev_x = ev.data();
+    cudaEvent_t* ev_in = ev.data() + nb;
+    cudaEvent_t* ev_c = ev.data() + 2 * nb;
+    const auto* xh = reinterpret_cast<const unsigned char*>(x.data);
+    auto* yh = reinterpret_cast<unsigned char*>(y.data);
+    auto* zh = chain ? reinterpret_cast<unsigned char*>(o.z->data) : nullptr;
+    const bool need_y = (o.flags & kFlagAxpby) != 0;
+    auto rows_of = [&](int b, gidx& r0, gidx& r1) {
+        r0 = std::min<gidx>(y.nrows, rgb[b] * 32);
+        r1 = std::min<gidx>(y.nrows, rgb[b + 1] * 32);
+    };
+    // x slabs (same row split as the blocks) and the per-block y/z inputs, in order
+    gidx xdone = 0;
+    std::vector<int> slab_for(static_cast<std::size_t>(nb));
+    for (int s = 0; s < nb; ++s) {
+        const gidx x1 = (s == nb - 1) ? gidx(x.nrows) : std::min<gidx>(x.nrows, gidx(x.nrows) * (s + 1) / nb);
+        if (x1 > xdone)
+            CK(cudaMemcpyAsync(xd + std::size_t(xdone) * xrow, xh + std::size_t(xdone) * xrow,
+                               std::size_t(x1 - xdone) * xrow, cudaMemcpyHostToDevice, rt.h2d));
+        CK(cudaEventRecord(ev_x[s], rt.h2d));
+        gidx r0, r1;
+        rows_of(s, r0, r1);
+        if (need_y && r1 > r0)
+            CK(cudaMemcpyAsync(yd + std::size_t(r0) * xrow, yh + std::size_t(r0) * xrow, std::size_t(r1 - r0) * xrow,
+                               cudaMemcpyHostToDevice, rt.h2d));
+        if (chain && r1 > r0)
+            CK(cudaMemcpyAsync(zd + std::size_t(r0) * xrow, zh + std::size_t(r0) * xrow, std::size_t(r1 - r0) * xrow,
+                               cudaMemcpyHostToDevice, rt.h2d));
+        CK(cudaEventRecord(ev_in[s], rt.h2d));
+        xdone = x1;
+    }
+    for (int b = 0; b < nb; ++b) {
+        int s = 0;  // first slab that contains the block's watermark row
+        while (s < nb - 1 && std::min<gidx>(x.nrows, gidx(x.nrows) * (s + 1) / nb) <= gidx(A.watermark[b])) ++s;
+        slab_for[b] = std::max(s, b);  // y/z inputs of block b arrive with slab b
+    }
+    const bool dots = (o.flags & kFlagDots) != 0;
+    SpmvOptions run = o;
+    run.z = chain ? &zdev : nullptr;
+    run.dot = nullptr;
+    DeviceBuffer dots_buf(dots ? 3 * std::size_t(w) * es : 16, A.device);
+    if (dots) CK(cudaMemsetAsync(dots_buf.get(), 0, 3 * std::size_t(w) * es, rt.stream));
+    for (int b = 0; b < nb; ++b) {
+        CK(cudaStreamWaitEvent(rt.stream, ev_in[slab_for[b]], 0));
+        SpmvHooks h;
+        h.rg0 = rgb[b];
+        h.rg1 = rgb[b + 1];
+        h.accumulate_dots = dots;
+        h.dot_accum = dots_buf.get();
+        spmv_device(ydev, A, xdev, run, h);
+        CK(cudaEventRecord(ev_c[b], rt.stream));
+        CK(cudaStreamWaitEvent(rt.d2h, ev_c[b], 0));
+        gidx r0, r1;
+        rows_of(b, r0, r1);
+        if (r1 > r0) {
+            CK(cudaMemcpyAsync(yh + std::size_t(r0) * xrow, yd + std::size_t(r0) * xrow, std::size_t(r1 - r0) * xrow,
+                               cudaMemcpyDeviceToHost, rt.d2h));
+            if (chain)
+                CK(cudaMemcpyAsync(zh + std::size_t(r0) * xrow, zd + std::size_t(r0) * xrow,
+                                   std::size_t(r1 - r0) * xrow, cudaMemcpyDeviceToHost, rt.d2h));
+        }
+    }
+    if (dots) {
+        for (int s = 0; s < 3; ++s)
+            if (o.flags & (kFlagDotYY << s))
+                CK(cudaMemcpyAsync(static_cast<unsigned char*>(o.dot) + std::size_t(s) * w * es,
+                                   static_cast<unsigned char*>(dots_buf.get()) + std::size_t(s) * w * es, w * es,
+                                   cudaMemcpyDefault, rt.stream));
+    }
+    CK(cudaStreamSynchronize(rt.stream));
+    CK(cudaStreamSynchronize(rt.d2h));
+    CK(cudaStreamSynchronize(rt.h2d));
+    for (auto& e : ev) cudaEventDestroy(e);
+    return true;
+}
 
 void spmv_options_from(Datatype dt, std::uint32_t flags, const void* alpha, const void* beta, const void* gamma,
                        const void* delta, const void* eta, SpmvOptions& o) {
@@ -112,6 +257,8 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         a.eta = scalar_of<T>(o.eta);
         a.defer_mask = hooks.defer_mask;
         a.row_map = hooks.row_map;
+        a.rg0 = hooks.rg0;
+        a.rg1 = hooks.rg1 < 0 ? (gidx(A.nrows_padded) + 31) / 32 : hooks.rg1;
 
         // scratch: [gamma_list W][final dots 3W][partials]
         const std::size_t max_parts = std::size_t(rt.num_sms) * 32 * std::size_t((W + kGW - 1) / kGW + 1);
@@ -170,6 +317,7 @@ void spmv(DenseMat& y, const SellMat& A, const DenseMat& x_in, const SpmvOptions
 
     DeviceGuard g(A.device);
     auto& rt = runtime(A.device);
+    if (x.mem == MemKind::host && y.mem == MemKind::host && spmv_host_streamed(y, A, x, o)) return;
     Staged xs(x, true);
     Staged ys(y, (f & kFlagAxpby) != 0);
     DenseMat zdummy;

@@ -52,6 +52,7 @@ struct SpmvHooks {
     void* dot_accum = nullptr;     // device, 3*width
     cudaStream_t stream = nullptr; // override the runtime stream
     const DenseMat* x_self = nullptr;  // x of the output rows for shift/dots when x is a halo block
+    gidx rg0 = 0, rg1 = -1;            // row groups (32 stored rows) to sweep; rg1 < 0: all
 };
 
 // Validation (spmv.hpp:98-125) + launch.  y/x/z may be host-resident views.

@@ -67,6 +67,7 @@ struct KArgs {
     T* partial;
     const std::uint32_t* defer_mask;
     const lidx* row_map;
+    gidx rg0, rg1;  // row groups (32 stored rows each) [rg0, rg1) swept by this launch
 };
 
 namespace spmv_detail {
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kBlock) spmv_cw_kernel(const KArgs<T> a) {
     const int sub = lane % TPR;
     const int rsub = lane / TPR;
     const int col_base = slice * WS;
-    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx ngroups = a.rg1;
     const bool want_dots = (a.flags & kFlagDots) != 0;
     const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
     const unsigned long long pol = l2_evict_first_policy();
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kBlock) spmv_cw_kernel(const KArgs<T> a) {
 #pragma unroll
             for (int e = 0; e < VEC; ++e) dsum[s][q][e] = O::zero();
 
-    for (gidx rg = gw / NSLICE; rg < ngroups; rg += tw / NSLICE) {
+    for (gidx rg = a.rg0 + gw / NSLICE; rg < ngroups; rg += tw / NSLICE) {
         const gidx r_own = rg * 32 + lane;
         const gidx c_own = r_own / C;
         const lidx i_own = lidx(r_own - c_own * C);
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
     }
     __syncthreads();
     const int chunks_per_tile = rgt * (32 / C);
-    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx ngroups = a.rg1;
     const bool want_dots = (a.flags & kFlagDots) != 0;
 
     if (warp == kNCW) {
@@ -469,8 +470,8 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
             mbar_wait(&empty[s], (k & 1u) ^ 1u);
-            const gidx c0 = t * chunks_per_tile;
-            const gidx c1 = min(a.nchunks, c0 + chunks_per_tile);
+            const gidx c0 = a.rg0 * (32 / C) + t * chunks_per_tile;
+            const gidx c1 = min(min(a.nchunks, a.rg1 * (32 / C)), c0 + chunks_per_tile);
             const int nc = int(c1 - c0);
             const gidx off0 = a.chunk_offset[c0];
             for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
             mbar_wait(&full[s], k & 1u);
-            const gidx rg = t * rgt + rgi;
+            const gidx rg = a.rg0 + t * rgt + rgi;
             if (rgi < rgt && rg < ngroups) {
                 T acc[TPR][NV][VEC];
                 const T* sval = reinterpret_cast<const T*>(smem + s * SB);
@@ -621,7 +622,9 @@ __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const KArgs<T> a) 
 #pragma unroll
         for (int e = 0; e < kGW; ++e) dsum[s][e] = O::zero();
 
-    for (gidx r = blockIdx.x * gidx(blockDim.x) + threadIdx.x; r < a.nrows; r += gidx(gridDim.x) * blockDim.x) {
+    const gidx r_end = min(gidx(a.nrows), a.rg1 * 32);
+    for (gidx r = a.rg0 * 32 + blockIdx.x * gidx(blockDim.x) + threadIdx.x; r < r_end;
+         r += gidx(gridDim.x) * blockDim.x) {
         const gidx c = r / a.C;
         const lidx i = lidx(r - c * a.C);
         const gidx off = a.chunk_offset[c];
@@ -745,7 +748,7 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, tma_smem_bytes<T, W>()));
         return std::max(nb, 1);
     }();
-    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx ngroups = a.rg1 - a.rg0;
     const gidx ntiles = (ngroups + rgt - 1) / rgt;
     const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
     static const int seg = [] {
@@ -768,7 +771,7 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
     }
     auto kern = spmv_cw_kernel<T, C, W, U>;
     const int per_sm = occupancy_blocks(kern);
-    const gidx ngroups = (gidx(a.nrows_padded) + 31) / 32;
+    const gidx ngroups = a.rg1 - a.rg0;
     const gidx items = ngroups * P::NSLICE;
     const gidx need = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int grid = int(std::max<gidx>(1, std::min<gidx>(need, gidx(per_sm) * rt.num_sms)));
@@ -779,7 +782,7 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
 template <class T>
 LaunchShape launch_generic(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st) {
     const int ncb = (a.width + kGW - 1) / kGW;
-    const gidx need = (gidx(a.nrows) + kBlock - 1) / kBlock;
+    const gidx need = ((a.rg1 - a.rg0) * 32 + kBlock - 1) / kBlock;
     const int gx = int(std::max<gidx>(1, std::min<gidx>(need, gidx(rt.num_sms) * 8)));
     spmv_generic_kernel<T><<<dim3(gx, ncb), kBlock, 0, st>>>(a);
     return {gx, gx, 1};

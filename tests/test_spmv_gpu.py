@@ -190,6 +190,33 @@ def test_col_major_and_host_views(sk, orc):
     assert np.array_equal(yh, yo)
 
 
+@pytest.mark.parametrize("w", [1, 8])
+def test_streamed_pinned_host_buffers(sk, orc, w):
+    """sellkit_spmv on pinned host views streams x in / y out by row blocks (column
+    watermarks); results are bit-identical to the resident path and the oracle."""
+    import torch
+    n = 40
+    N = n ** 3
+    rp, c, v = stencil_crs(7, n)
+    A = sk.crs_stencil(7, n).build(32, 256)
+    Ao = orc.build(rp, c, v, 32, 256)
+    xv, y0, z0 = hash_block(N, w, 11), hash_block(N, w, 12), hash_block(N, w, 13)
+    bufs = {}
+    for name, arr in [("x", xv), ("y", y0), ("z", z0)]:
+        t = torch.empty((N, w), dtype=torch.float64, pin_memory=True)
+        t.copy_(torch.from_numpy(arr))
+        bufs[name] = t
+    views = {k: sk.view_plain(t.data_ptr(), N * w, N, w, w, keep=t) for k, t in bufs.items()}
+    flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.CHAIN_AXPBY
+    dots = np.zeros(3 * w)
+    sk.spmv(views["y"], A, views["x"], flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, delta=1.0, eta=0.3,
+            z=views["z"], dot=dots)
+    yo, zo, do = orc.spmv(Ao, xv, y0, z0, flags, alpha=0.5, beta=-1.0, gamma=0.25, delta=1.0, eta=0.3)
+    assert np.array_equal(bufs["y"].numpy(), yo)
+    assert np.array_equal(bufs["z"].numpy(), zo)
+    assert np.all(np.abs(dots[:2 * w] - do[:2 * w]) <= 1e-12 * (1 + np.abs(do[:2 * w])))
+
+
 def test_spmv_validation(sk):
     I = sk.crs(np.arange(4), np.arange(3), np.ones(3)).build(1, 1)
     x, y = sk.densemat(3, 1), sk.densemat(3, 1)
