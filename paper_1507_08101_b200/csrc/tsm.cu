@@ -211,6 +211,195 @@ __global__ void gemm_naive_kernel(DAcc c, DAcc a, DAcc b, lidx n, lidx kc, lidx 
     cr = O::add(O::mul(alpha, s), O::mul(beta, cr));
 }
 
+// ---------------------------------------------------------------- fast paths
+// Row-major, compact V/W (column step 1, no column map), real element types.
+
+// TSMTTSM, m <= MM, k <= KK (MM, KK in {1,2,4,8}): each thread keeps the whole
+// m x k block in registers and walks its rows of the CTA's contiguous range;
+// warp butterfly + ordered CTA sum -> one partial per CTA (deterministic).
+template <class T, int MM, int KK, bool KAHAN>
+__global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v, gidx vs, const T* __restrict__ w,
+                                                         gidx ws, gidx n, int m, int k, gidx rows_per_cta, T* partial,
+                                                         T* pcomp) {
+    using O = Ops<T>;
+    __shared__ T red[kT / 32][MM * KK];
+    __shared__ T redc[KAHAN ? kT / 32 : 1][MM * KK];
+    T acc[MM][KK], cmp[MM][KK];
+#pragma unroll
+    for (int a = 0; a < MM; ++a)
+#pragma unroll
+        for (int b = 0; b < KK; ++b) acc[a][b] = cmp[a][b] = O::zero();
+    const gidx r0 = gidx(blockIdx.x) * rows_per_cta;
+    const gidx r1 = min(n, r0 + rows_per_cta);
+    for (gidx i = r0 + threadIdx.x; i < r1; i += kT) {
+        T vr[MM], wr[KK];
+#pragma unroll
+        for (int a = 0; a < MM; ++a) vr[a] = a < m ? O::conj(__ldg(v + i * vs + a)) : O::zero();
+#pragma unroll
+        for (int b = 0; b < KK; ++b) wr[b] = b < k ? __ldg(w + i * ws + b) : O::zero();
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int b = 0; b < KK; ++b) {
+                if constexpr (KAHAN) kbn_add(acc[a][b], cmp[a][b], O::mul(vr[a], wr[b]));
+                else acc[a][b] = O::fma(vr[a], wr[b], acc[a][b]);
+            }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < MM; ++a)
+#pragma unroll
+        for (int b = 0; b < KK; ++b)
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                if constexpr (KAHAN) {
+                    // combine (sum, comp) pairs of two lanes compensatedly
+                    const T os = shfl_xor(acc[a][b], s), oc = shfl_xor(cmp[a][b], s);
+                    T ss = acc[a][b], cc = cmp[a][b];
+                    kbn_add(ss, cc, os);
+                    kbn_add(ss, cc, oc);
+                    acc[a][b] = ss;
+                    cmp[a][b] = cc;
+                } else {
+                    acc[a][b] = O::add(acc[a][b], shfl_xor(acc[a][b], s));
+                }
+            }
+    if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int b = 0; b < KK; ++b) {
+                red[warp][b * MM + a] = acc[a][b];
+                if constexpr (KAHAN) redc[warp][b * MM + a] = cmp[a][b];
+            }
+    }
+    __syncthreads();
+    if (int(threadIdx.x) < MM * KK) {
+        const int a = threadIdx.x % MM, b = threadIdx.x / MM;
+        if (a < m && b < k) {
+            T s = O::zero(), c = O::zero();
+            for (int q = 0; q < kT / 32; ++q) {
+                if constexpr (KAHAN) {
+                    kbn_add(s, c, red[q][threadIdx.x]);
+                    kbn_add(s, c, redc[q][threadIdx.x]);
+                } else {
+                    s = O::add(s, red[q][threadIdx.x]);
+                }
+            }
+            const gidx cell = gidx(b) * m + a;  // col-major m x k like tsm.hpp:145
+            partial[gidx(blockIdx.x) * m * k + cell] = s;
+            if constexpr (KAHAN) pcomp[gidx(blockIdx.x) * m * k + cell] = c;
+        }
+    }
+}
+
+// TSMTTSM, general sizes: rows staged in shared memory 64 at a time (coalesced,
+// contiguous copy when V/W are compact), each thread owns a TM x TK tile of cells.
+template <class T, int TM, int TK, bool KAHAN>
+__global__ void __launch_bounds__(kT) tsmttsm_tile_kernel(const T* __restrict__ v, gidx vs, const T* __restrict__ w,
+                                                          gidx ws, gidx n, int m, int k, gidx rows_per_cta, T* partial,
+                                                          T* pcomp) {
+    using O = Ops<T>;
+    constexpr int RT = 64;
+    extern __shared__ unsigned char smem_raw[];
+    T* vsm = reinterpret_cast<T*>(smem_raw);  // [RT][m]
+    T* wsm = vsm + RT * m;                     // [RT][k]
+    const int tm = (m + TM - 1) / TM, tk = (k + TK - 1) / TK;
+    const int tid = threadIdx.x + blockIdx.y * kT;  // cell tile index
+    const bool active = tid < tm * tk;
+    const int a0 = (tid % tm) * TM, b0 = (tid / tm) * TK;
+    T acc[TM][TK], cmp[TM][TK];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TK; ++b) acc[a][b] = cmp[a][b] = O::zero();
+    const gidx r0 = gidx(blockIdx.x) * rows_per_cta;
+    const gidx r1 = min(n, r0 + rows_per_cta);
+    for (gidx rb = r0; rb < r1; rb += RT) {
+        const int nr = int(min(gidx(RT), r1 - rb));
+        __syncthreads();
+        for (int t = threadIdx.x; t < nr * m; t += kT) vsm[t] = O::conj(v[(rb + t / m) * vs + t % m]);
+        for (int t = threadIdx.x; t < nr * k; t += kT) wsm[t] = w[(rb + t / k) * ws + t % k];
+        __syncthreads();
+        if (!active) continue;
+        for (int r = 0; r < nr; ++r) {
+            T va[TM], wb[TK];
+#pragma unroll
+            for (int a = 0; a < TM; ++a) va[a] = a0 + a < m ? vsm[r * m + a0 + a] : O::zero();
+#pragma unroll
+            for (int b = 0; b < TK; ++b) wb[b] = b0 + b < k ? wsm[r * k + b0 + b] : O::zero();
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TK; ++b) {
+                    if constexpr (KAHAN) kbn_add(acc[a][b], cmp[a][b], O::mul(va[a], wb[b]));
+                    else acc[a][b] = O::fma(va[a], wb[b], acc[a][b]);
+                }
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TK; ++b)
+            if (a0 + a < m && b0 + b < k) {
+                const gidx cell = gidx(b0 + b) * m + a0 + a;
+                partial[gidx(blockIdx.x) * m * k + cell] = acc[a][b];
+                if constexpr (KAHAN) pcomp[gidx(blockIdx.x) * m * k + cell] = cmp[a][b];
+            }
+}
+
+// TSMM, row-major V/W: a thread computes RT rows x KT columns of W; X (m x k,
+// row-major) lives in shared memory.  EXACT keeps the reference's rounding
+// (separate mul/add, m ascending) for the bandwidth-bound shapes.
+template <class T, int RT, int KT, bool EXACT>
+__global__ void __launch_bounds__(kT) tsmm_tile_kernel(T* __restrict__ w, gidx ws, const T* __restrict__ v, gidx vs,
+                                                       const T* __restrict__ xcm, gidx n, int m, int k, T alpha, T beta,
+                                                       int beta_zero) {
+    using O = Ops<T>;
+    extern __shared__ unsigned char smem_raw[];
+    T* xs = reinterpret_cast<T*>(smem_raw);  // row-major [m][k]
+    for (int t = threadIdx.x; t < m * k; t += kT) xs[t] = xcm[gidx(t % k) * m + t / k];
+    __syncthreads();
+    const int nkb = (k + KT - 1) / KT;
+    const gidx nrb = (n + RT - 1) / RT;
+    const gidx items = nrb * nkb;
+    for (gidx it = blockIdx.x * gidx(kT) + threadIdx.x; it < items; it += gidx(gridDim.x) * kT) {
+        const gidx rb = it / nkb;
+        const int kb = int(it - rb * nkb);
+        const gidx i0 = rb * RT;
+        const int c0 = kb * KT;
+        T tmp[RT][KT];
+#pragma unroll
+        for (int r = 0; r < RT; ++r)
+#pragma unroll
+            for (int e = 0; e < KT; ++e) tmp[r][e] = O::zero();
+        for (int mm = 0; mm < m; ++mm) {
+            T vr[RT], xk[KT];
+#pragma unroll
+            for (int r = 0; r < RT; ++r) vr[r] = i0 + r < n ? __ldg(v + (i0 + r) * vs + mm) : O::zero();
+#pragma unroll
+            for (int e = 0; e < KT; ++e) xk[e] = c0 + e < k ? xs[mm * k + c0 + e] : O::zero();
+#pragma unroll
+            for (int r = 0; r < RT; ++r)
+#pragma unroll
+                for (int e = 0; e < KT; ++e) tmp[r][e] = madd<T, EXACT>(tmp[r][e], vr[r], xk[e]);
+        }
+#pragma unroll
+        for (int r = 0; r < RT; ++r) {
+            if (i0 + r >= n) break;
+#pragma unroll
+            for (int e = 0; e < KT; ++e) {
+                if (c0 + e >= k) break;
+                T* wp = w + (i0 + r) * ws + c0 + e;
+                *wp = beta_zero ? O::mul(alpha, tmp[r][e]) : O::add(O::mul(alpha, tmp[r][e]), O::mul(beta, *wp));
+            }
+        }
+    }
+}
+
+bool compact_rows(const DenseMat& m) { return !m.scattered() && m.order == Order::row_major; }
+
 template <class T>
 T scalar_or(const void* p, T dflt) {
     if (!p) return dflt;
@@ -253,8 +442,74 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
     const lidx m = x.nrows, k = x.ncols;
     const gidx n = v.nrows;
     const gidx cells = gidx(m) * k;
-    const int cell_tiles = int((cells + kT * kCellsPerThread - 1) / (kT * kCellsPerThread));
     const std::size_t es = x.esize();
+    if (!is_complex(x.dt) && compact_rows(vs.dev) && compact_rows(wsg.dev) && n > 0) {
+        const int nparts = int(std::max<gidx>(1, std::min<gidx>(gidx(rt.num_sms) * 4, (n + 255) / 256)));
+        const gidx rows_per = (n + nparts - 1) / nparts;
+        auto* part = static_cast<unsigned char*>(rt.scratch_bytes(std::size_t(nparts) * cells * es * 2 + 256));
+        DAcc xa = dacc(xs.dev);
+        auto p2 = [](int q) { return q <= 1 ? 1 : q <= 2 ? 2 : q <= 4 ? 4 : 8; };
+        visit_dt(x.dt, [&]<class T>() {
+            if constexpr (!scalar_traits<T>::is_complex) {
+                T* p = reinterpret_cast<T*>(part);
+                T* pc = p + std::size_t(nparts) * cells;
+                const T a = scalar_or<T>(alpha, Ops<T>::one()), b = scalar_or<T>(beta, Ops<T>::zero());
+                const T* vp = reinterpret_cast<const T*>(vs.dev.data);
+                const T* wp = reinterpret_cast<const T*>(wsg.dev.data);
+                const gidx vst = vs.dev.stride, wst = wsg.dev.stride;
+                if (m <= 8 && k <= 8) {
+                    auto go = [&]<int MM, int KK>() {
+                        if (kahan) tsmttsm_reg_kernel<T, MM, KK, true><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
+                        else tsmttsm_reg_kernel<T, MM, KK, false><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
+                    };
+                    auto gok = [&]<int MM>() {
+                        switch (p2(k)) {
+                            case 1: go.template operator()<MM, 1>(); break;
+                            case 2: go.template operator()<MM, 2>(); break;
+                            case 4: go.template operator()<MM, 4>(); break;
+                            default: go.template operator()<MM, 8>(); break;
+                        }
+                    };
+                    switch (p2(m)) {
+                        case 1: gok.template operator()<1>(); break;
+                        case 2: gok.template operator()<2>(); break;
+                        case 4: gok.template operator()<4>(); break;
+                        default: gok.template operator()<8>(); break;
+                    }
+                } else {
+                    const std::size_t smem = 64 * std::size_t(m + k) * es;
+                    SK_REQUIRE(smem <= 200 * 1024, errc::unsupported, "tsmttsm: V/W rows too wide");
+                    auto go = [&]<int TM, int TK>() {
+                        const int tiles = ((m + TM - 1) / TM) * ((k + TK - 1) / TK);
+                        const dim3 grid(nparts, (tiles + kT - 1) / kT);
+                        if (kahan) {
+                            auto kern = tsmttsm_tile_kernel<T, TM, TK, true>;
+                            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                            kern<<<grid, kT, smem, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
+                        } else {
+                            auto kern = tsmttsm_tile_kernel<T, TM, TK, false>;
+                            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                            kern<<<grid, kT, smem, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
+                        }
+                    };
+                    if (cells <= 256) go.template operator()<1, 1>();
+                    else if (cells <= 1024) go.template operator()<2, 2>();
+                    else go.template operator()<4, 4>();
+                }
+                CK(cudaGetLastError());
+                if (kahan)
+                    tsmttsm_final_kernel<T, true><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, nparts, m, k, xa, a, b);
+                else
+                    tsmttsm_final_kernel<T, false><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, nparts, m, k, xa, a, b);
+            }
+            return 0;
+        });
+        CK(cudaGetLastError());
+        xs.write_back();
+        finish(rt);
+        return;
+    }
+    const int cell_tiles = int((cells + kT * kCellsPerThread - 1) / (kT * kCellsPerThread));
     // CTAs over rows: enough to fill the machine, rows per CTA a multiple of the tile
     const int want = std::max(1, rt.num_sms * 2 / cell_tiles);
     gidx rows_per = std::max<gidx>(kRowTile, (n + want - 1) / want);
@@ -308,10 +563,36 @@ void tsmm(DenseMat& w, const DenseMat& v_in, const DenseMat& x_in, const void* a
     const std::size_t xbytes = std::size_t(m) * k * es;
     const int x_in_smem = xbytes <= 96 * 1024 ? 1 : 0;
     const bool exact = gidx(m) * k <= 64;
+    const bool fast = !is_complex(w.dt) && compact_rows(vs.dev) && compact_rows(wsg.dev) && x_in_smem && n > 0;
     visit_dt(w.dt, [&]<class T>() {
         T* xc = reinterpret_cast<T*>(xcm);
         x_colmajor_kernel<T><<<int((gidx(m) * k + 255) / 256), 256, 0, rt.stream>>>(xa, m, k, xc);
         const T a = scalar_or<T>(alpha, Ops<T>::one()), b = scalar_or<T>(beta, Ops<T>::zero());
+        if constexpr (!scalar_traits<T>::is_complex) {
+            if (fast) {
+                T* wp = reinterpret_cast<T*>(wsg.dev.data);
+                const T* vp = reinterpret_cast<const T*>(vs.dev.data);
+                const gidx wst = wsg.dev.stride, vst = vs.dev.stride;
+                auto go = [&]<int RT, int KT, bool EX>() {
+                    auto kern = tsmm_tile_kernel<T, RT, KT, EX>;
+                    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(xbytes)));
+                    const gidx items = ((n + RT - 1) / RT) * ((k + KT - 1) / KT);
+                    const int grid = int(std::max<gidx>(1, std::min<gidx>((items + kT - 1) / kT, gidx(rt.num_sms) * 8)));
+                    kern<<<grid, kT, xbytes, rt.stream>>>(wp, wst, vp, vst, xc, n, m, k, a, b, beta_zero ? 1 : 0);
+                };
+                if (exact) {  // m*k <= 64: one thread per row, all k columns, reference rounding
+                    if (k <= 1) go.template operator()<1, 1, true>();
+                    else if (k <= 2) go.template operator()<1, 2, true>();
+                    else if (k <= 4) go.template operator()<1, 4, true>();
+                    else go.template operator()<1, 8, true>();
+                } else if (k <= 4) {
+                    go.template operator()<4, 4, false>();
+                } else {
+                    go.template operator()<4, 8, false>();
+                }
+                return 0;
+            }
+        }
         auto launch = [&](auto kern) {
             const std::size_t smem = x_in_smem ? xbytes : 0;
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max<std::size_t>(smem, 1))));

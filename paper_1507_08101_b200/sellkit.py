@@ -215,7 +215,9 @@ class Sellkit:
             raise SellkitError(code, where, self.lib.sellkit_error_name(code).decode())
 
     def call(self, name: str, *args):
-        code = getattr(self.lib, name)(*args)
+        """Call `name`; handle objects may be passed directly and stay alive for the call."""
+        raw = [a.h if isinstance(a, _Handle) else a for a in args]
+        code = getattr(self.lib, name)(*raw)
         self.check(code, name)
 
     # -- objects ------------------------------------------------------------

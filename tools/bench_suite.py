@@ -1,0 +1,108 @@
+#!/usr/bin/env python
+"""Secondary measurements (BASELINE.json configs other than the bench.py headline):
+
+  c1   SpMV SELL-32-1, 2-D 5-point 1000^2, w = 1 (L2 flushed between reps)
+  c2   SpMMV SELL-32-256, 3-D 7-point 256^3, w in {1, 4, 8, 16, 32} (+ AXPBY)
+  c4   TSMM / TSMTTSM, N = 1e8, m = k in {1, 2, 4, 8, 16, 32, 64}
+
+Device-resident inputs, CUDA events on the library stream, median of reps.
+One JSON line per case on stdout.  Usage: python tools/bench_suite.py [c1] [c2] [c4]
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1507_08101_b200 import sellkit  # noqa: E402
+
+sk = sellkit.load()
+stream = torch.cuda.ExternalStream(sk.stream())
+PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
+flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+
+def timed(fn, reps=10, warm=2, flush=False):
+    sk.set_sync(False)
+    for _ in range(warm):
+        fn()
+    sk.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush:
+            with torch.cuda.stream(stream):
+                flush_buf.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        sk.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    sk.set_sync(True)
+    return float(np.median(ts))
+
+
+def emit(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def spmv_case(tag, A, N, nnz, w, flags=0, flush=False, reps=10):
+    x = sk.densemat(N, w)
+    x.fill_hash(42)
+    y = sk.densemat(N, w)
+    if flags & sellkit.AXPBY:
+        y.fill_hash(43)
+    beta = np.array([0.5])
+
+    def fn():
+        if flags:
+            sk.spmv(y, A, x, flags=flags, beta=beta)
+        else:
+            sk.spmv(y, A, x)
+    ms = timed(fn, reps=reps, flush=flush)
+    alg = 12.0 * nnz + 8.0 * w * N * (2 + (1 if flags & sellkit.AXPBY else 0))
+    emit(case=tag, w=w, flags=flags, ms=ms, gflops=2.0 * nnz * w / ms / 1e6, gbs=alg / ms / 1e6,
+         frac=alg / ms / 1e6 / PEAK, l2_flushed=flush)
+
+
+def c1():
+    n = 1000
+    A = sk.crs_stencil(5, n).build(32, 1)
+    spmv_case("c1 5pt 1000^2 SELL-32-1", A, n * n, 5 * n * n - 4 * n, 1, flush=True, reps=30)
+
+
+def c2():
+    n = 256
+    A = sk.crs_stencil(7, n).build(32, 256)
+    nnz = 7 * n ** 3 - 6 * n ** 2
+    for w in (1, 4, 8, 16, 32):
+        spmv_case("c2 7pt 256^3 SELL-32-256", A, n ** 3, nnz, w)
+    spmv_case("c2 7pt 256^3 SELL-32-256", A, n ** 3, nnz, 8, flags=sellkit.AXPBY)
+
+
+def c4():
+    N = 100_000_000
+    for m in (1, 2, 4, 8, 16, 32, 64):
+        k = m
+        V, W, X = sk.densemat(N, m), sk.densemat(N, k), sk.densemat(m, k)
+        V.fill_hash(1)
+        W.fill_hash(2)
+        X.fill_hash(3)
+        one, zero = np.array([1.0]), np.array([0.0])
+        ms = timed(lambda: sk.call("sellkit_tsmm", W, V, X, one.ctypes.data, zero.ctypes.data), reps=5)
+        alg = 8.0 * N * (m + k)
+        emit(case="c4 tsmm N=1e8 beta=0", m=m, k=k, ms=ms, gflops=2.0 * N * m * k / ms / 1e6, gbs=alg / ms / 1e6,
+             frac=alg / ms / 1e6 / PEAK)
+        ms = timed(lambda: sk.call("sellkit_tsmttsm", X, V, W, one.ctypes.data, zero.ctypes.data, 0), reps=5)
+        emit(case="c4 tsmttsm N=1e8", m=m, k=k, ms=ms, gflops=2.0 * N * m * k / ms / 1e6, gbs=alg / ms / 1e6,
+             frac=alg / ms / 1e6 / PEAK)
+        del V, W, X
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1", "c2", "c4"]
+    for w in which:
+        globals()[w]()
