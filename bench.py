@@ -198,7 +198,9 @@ def run_ours(args, rank, world, local_rank):
     n, w = args.n, args.width
     N = n ** 3
     nnz_total = stencil_nnz(n)
-    if world > 1:
+    if world > 1 or os.environ.get("SELLKIT_BENCH_RANKCTX") == "1":
+        # one process per GPU: rank context (NCCL halo exchange); SELLKIT_BENCH_RANKCTX=1
+        # exercises the same path at world size 1
         from paper_1507_08101_b200 import dist as skdist
         job = skdist.bench_setup(sk, n, w, args.chunk, args.sigma, rank, world)
     else:
