@@ -42,6 +42,14 @@ sellkit_error sellkit_ext_crs_create_device(sellkit_datatype dt, sellkit_gidx nr
 sellkit_error sellkit_ext_crs_stencil(sellkit_datatype dt, int points, sellkit_gidx n,
                                       sellkit_gidx row_begin, sellkit_gidx row_end, sellkit_crs** out);
 
+/* Synthetic topological-insulator Hamiltonian: 4 orbitals per site
+ * of a periodic Lx x Ly x Lz lattice, 13 nonzeros per row (on-site 2*G1 + V*I, six
+ * hoppings (G1 -/+ i*G_{a+2})/2 with Dirac matrices G1 = tau_z(x)I, G2..G4 =
+ * tau_x(x)sigma_{x,y,z}); V uniform in [-disorder/2, disorder/2) from a site hash.
+ * Real datatypes get the real parts (same sparsity pattern).  Rows [row_begin, row_end). */
+sellkit_error sellkit_ext_crs_ti(sellkit_datatype dt, sellkit_gidx lx, sellkit_gidx ly, sellkit_gidx lz,
+                                 double disorder, sellkit_gidx row_begin, sellkit_gidx row_end, sellkit_crs** out);
+
 /* -------------------------------------------------------- layout export -- */
 sellkit_error sellkit_ext_mat_info(const sellkit_mat* m, int* chunk_height, int* sigma,
                                    sellkit_lidx* nrows_padded, sellkit_gidx* nchunks,

@@ -244,6 +244,51 @@ def stencil_box(nx: int, ny: int, nz: int):
     return rowptr, col.astype(np.int64), val.astype(np.float64)
 
 
+def ti_crs(lx: int, ly: int, lz: int, disorder: float = 0.0):
+    """Numpy restatement of the synthetic topological-insulator Hamiltonian of
+    sellkit_ext_crs_ti: 4 orbitals per periodic site, 13 nonzeros per
+    row: on-site 2*G1 + V*I and hoppings (G1 -/+ i*G_{a+2})/2, G1 = tau_z(x)I,
+    G2..4 = tau_x(x)sigma_{x,y,z}."""
+    nsite = lx * ly * lz
+    rows = np.arange(4 * nsite, dtype=np.int64)
+    site, o = rows >> 2, rows & 3
+    x, y, z = site % lx, (site // lx) % ly, site // (lx * ly)
+    g1 = np.where(o < 2, 1.0, -1.0)
+    with np.errstate(over="ignore"):
+        h = splitmix64(np.uint64(0x51) ^ site.astype(np.uint64))
+    u = (h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 - 0.5
+    cols = [rows]
+    vals = [2.0 * g1 + disorder * u + 0j]
+    to, so = o ^ 2, o & 1
+    for a in range(3):
+        for s in (-1, 1):
+            nx, ny, nz = x.copy(), y.copy(), z.copy()
+            if a == 0:
+                nx = (x + s) % lx
+            elif a == 1:
+                ny = (y + s) % ly
+            else:
+                nz = (z + s) % lz
+            ns = (nz * ly + ny) * lx + nx
+            cols.append(ns * 4 + o)
+            vals.append(0.5 * g1 + 0j)
+            if a == 0:
+                op, mr, mi = to ^ 1, np.ones(len(rows)), np.zeros(len(rows))
+            elif a == 1:
+                op, mr, mi = to ^ 1, np.zeros(len(rows)), np.where(so == 0, -1.0, 1.0)
+            else:
+                op, mr, mi = to, np.where(so == 0, 1.0, -1.0), np.zeros(len(rows))
+            cols.append(ns * 4 + op)
+            vals.append((-s * (-mi) * 0.5) + 1j * (-s * mr * 0.5))
+    C_ = np.stack(cols, 1)
+    V_ = np.stack(vals, 1)
+    order = np.argsort(C_, axis=1, kind="stable")
+    C_ = np.take_along_axis(C_, order, 1)
+    V_ = np.take_along_axis(V_, order, 1)
+    rowptr = np.arange(0, 13 * len(rows) + 1, 13, dtype=np.int64)
+    return rowptr, C_.reshape(-1), V_.reshape(-1)
+
+
 def random_crs(rng: np.random.Generator, nrows: int, ncols: int, density: float, cplx: bool = False):
     """Random CRS with >= 1 entry per row, columns ascending, values U(-1,1)
     (the shape of proj/tests/oracles.hpp:91-119)."""

@@ -21,6 +21,7 @@
 
 namespace skb {
 std::unique_ptr<Crs> crs_stencil(Datatype dt, int points, gidx n, gidx rb, gidx re);
+std::unique_ptr<Crs> crs_ti(Datatype dt, gidx Lx, gidx Ly, gidx Lz, double disorder, gidx rb, gidx re);
 void densemat_fill_hash(DenseMat& m, unsigned long long seed);
 void crs_validate_impl(const Crs& a, bool check_sorted);
 std::unique_ptr<Crs> crs_read_mm(const char* path, Datatype dt);
@@ -651,6 +652,14 @@ sellkit_error sellkit_ext_crs_stencil(sellkit_datatype dt, int points, sellkit_g
     return guarded([&] {
         require(out != nullptr, "null output");
         *out = new sellkit_crs{sk::crs_stencil(dt_from(dt), points, n, row_begin, row_end)};
+    });
+}
+
+sellkit_error sellkit_ext_crs_ti(sellkit_datatype dt, sellkit_gidx lx, sellkit_gidx ly, sellkit_gidx lz,
+                                 double disorder, sellkit_gidx row_begin, sellkit_gidx row_end, sellkit_crs** out) {
+    return guarded([&] {
+        require(out != nullptr, "null output");
+        *out = new sellkit_crs{sk::crs_ti(dt_from(dt), lx, ly, lz, disorder, row_begin, row_end)};
     });
 }
 

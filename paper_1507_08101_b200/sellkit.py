@@ -148,6 +148,7 @@ _EXT = [
     ("sellkit_ext_device_info", err_t, [C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
     ("sellkit_ext_crs_create_device", err_t, [C.c_int, gidx, gidx, vp, vp, vp, C.POINTER(vp)]),
     ("sellkit_ext_crs_stencil", err_t, [C.c_int, C.c_int, gidx, gidx, gidx, C.POINTER(vp)]),
+    ("sellkit_ext_crs_ti", err_t, [C.c_int, gidx, gidx, gidx, C.c_double, gidx, gidx, C.POINTER(vp)]),
     ("sellkit_ext_mat_info", err_t, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(lidx), C.POINTER(gidx),
                                      C.POINTER(gidx), C.POINTER(C.c_int)]),
     ("sellkit_ext_mat_export", err_t, [vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -237,6 +238,14 @@ class Sellkit:
         N = n * n if points == 5 else n ** 3
         out = vp()
         self.call("sellkit_ext_crs_stencil", dt, points, n, row_begin, N if row_end is None else row_end, C.byref(out))
+        return Crs(self, out, dt)
+
+    def crs_ti(self, lx: int, ly: int, lz: int, disorder: float = 0.0, row_begin: int = 0,
+               row_end: Optional[int] = None, dt=C64) -> "Crs":
+        N = 4 * lx * ly * lz
+        out = vp()
+        self.call("sellkit_ext_crs_ti", dt, lx, ly, lz, disorder, row_begin, N if row_end is None else row_end,
+                  C.byref(out))
         return Crs(self, out, dt)
 
     def densemat(self, nrows: int, ncols: int, dt=R64, order=ROW_MAJOR) -> "DenseMat":

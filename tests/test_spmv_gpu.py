@@ -154,6 +154,36 @@ def test_complex_vs_oracle(sk, orc):
         assert np.allclose(dots, do, rtol=1e-12, atol=1e-12)
 
 
+def test_ti_generator_and_kpm_step(sk, orc):
+    """C3: the device TI Hamiltonian equals the numpy restatement; the augmented KPM
+    step y = 2a(H - bI)x - y with <y,y>, <x,y>, <x,x> (w = 16, complex) is bit-identical
+    to the oracle in y and within 1e-12 in the dots."""
+    from oracle.oracle import ti_crs
+    lx, ly, lz, dis = 8, 6, 5, 0.7
+    rp, c, v = ti_crs(lx, ly, lz, dis)
+    n = len(rp) - 1
+    for dt in (sellkit.C64, sellkit.R64):
+        vv = v if dt == sellkit.C64 else v.real.copy()
+        A = sk.crs_ti(lx, ly, lz, dis, dt=dt).build(32, 128)
+        Ao = orc.build(rp, c, vv, 32, 128).layout()
+        L = A.export()
+        for key in LAYOUT_KEYS:
+            assert np.array_equal(L[key], Ao[key]), (dt, key)
+    A = sk.crs_ti(lx, ly, lz, dis).build(32, 128)
+    Ao = orc.build(rp, c, v, 32, 128)
+    rng = np.random.default_rng(4)
+    w = 16
+    xv = rng.uniform(-1, 1, (n, w)) + 1j * rng.uniform(-1, 1, (n, w))
+    y0 = rng.uniform(-1, 1, (n, w)) + 1j * rng.uniform(-1, 1, (n, w))
+    x, y = sk.densemat_from(xv), sk.densemat_from(y0)
+    dots = np.zeros(3 * w, np.complex128)
+    flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX
+    sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, dot=dots)
+    yo, _, do = orc.spmv(Ao, xv, y0, None, flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    assert np.array_equal(y.copy_out(), yo)
+    assert np.allclose(dots, do, rtol=1e-12, atol=1e-12)
+
+
 def test_single_precision(sk, orc):
     rng = np.random.default_rng(9)
     rp, c, v = random_crs(rng, 200, 200, 0.05)

@@ -83,6 +83,32 @@ def c2():
     spmv_case("c2 7pt 256^3 SELL-32-256", A, n ** 3, nnz, 8, flags=sellkit.AXPBY)
 
 
+def c3():
+    """Augmented KPM step on the synthetic TI Hamiltonian, 2^24 rows, w = 16:
+    y = 2a(H - bI)x - y with <y,y>, <x,y>, <x,x> (a = 0.25, b = 0.25); C64 and the
+    real-valued surrogate with the same pattern."""
+    lx, ly, lz = 256, 128, 128
+    N = 4 * lx * ly * lz
+    for dt, vb in ((sellkit.C64, 16), (sellkit.R64, 8)):
+        A = sk.crs_ti(lx, ly, lz, 1.0, dt=dt).build(32, 256)
+        nnz = 13 * N
+        w = 16
+        x, y = sk.densemat(N, w, dt), sk.densemat(N, w, dt)
+        x.fill_hash(42)
+        y.fill_hash(43)
+        dots = np.zeros(3 * w, sellkit.NP_DTYPE[dt])
+        flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX
+
+        def fn():
+            sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, dot=dots)
+        ms = timed(fn, reps=5)
+        alg = (vb + 4.0) * nnz + vb * w * N * 3  # x read, y read + write
+        fl = (8.0 if dt == sellkit.C64 else 2.0) * nnz * w
+        emit(case=f"c3 TI KPM step 2^24 rows w=16 {'C64' if dt == sellkit.C64 else 'R64'}", ms=ms,
+             gflops=fl / ms / 1e6, gbs=alg / ms / 1e6, frac=alg / ms / 1e6 / PEAK)
+        del A, x, y
+
+
 def c4():
     N = 100_000_000
     for m in (1, 2, 4, 8, 16, 32, 64):
