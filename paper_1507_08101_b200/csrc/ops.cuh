@@ -148,9 +148,7 @@ __device__ __forceinline__ Vec<T, N> ld_x(const T* p) {
     constexpr int B = int(sizeof(T)) * N;
     if constexpr (B == 32) {
         unsigned long long a, b, c, d;
-        asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
-                     : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
-                     : "l"(p));
+        asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
         unsigned long long tmp[4] = {a, b, c, d};
         memcpy(&r, tmp, 32);
     } else if constexpr (B == 4 || B == 8 || B == 16) {
@@ -203,6 +201,36 @@ __device__ __forceinline__ void st_vec(T* p, const Vec<T, N>& v) {
 #pragma unroll
         for (int i = 0; i < N; ++i) p[i] = v.v[i];
     }
+}
+
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// 32-byte RHS gather with an L2 eviction-priority hint (x rows are re-read by the
+// neighbouring rows of the sweep; the matrix and y stream past them).
+template <class T, int N>
+__device__ __forceinline__ Vec<T, N> ld_x_hint(const T* p, unsigned long long pol) {
+    static_assert(int(sizeof(T)) * N == 32, "32-byte gathers only");
+    Vec<T, N> r;
+    unsigned long long t[4];
+    asm("ld.global.nc.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=l"(t[0]), "=l"(t[1]), "=l"(t[2]), "=l"(t[3])
+        : "l"(p), "l"(pol));
+    memcpy(&r, t, 32);
+    return r;
+}
+
+template <class T, int N>
+__device__ __forceinline__ void st_vec_hint(T* p, const Vec<T, N>& v, unsigned long long pol) {
+    static_assert(int(sizeof(T)) * N == 32, "32-byte stores only");
+    unsigned long long t[4];
+    memcpy(t, &v, 32);
+    asm volatile("st.global.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "l"(t[0]), "l"(t[1]), "l"(t[2]),
+                 "l"(t[3]), "l"(pol)
+                 : "memory");
 }
 
 template <class T>

@@ -604,6 +604,246 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
     }
 }
 
+// ---------------------------------------------------------------------------
+// Row-contiguous variant of the TMA kernel (production path for RHS rows of
+// 32..256 bytes).  A lane owns ONE row and VEC = 32/sizeof(T) consecutive columns;
+// the TPR = W/VEC lanes of a row cover the whole RHS row, so one LDG.256 warp
+// instruction reads WR = 32/TPR complete, contiguous RHS rows (full 128-B lines):
+// half the L1 wavefronts of splitting the columns over warps, with only VEC
+// accumulators per lane, which leaves the registers for a deep gather unroll.
+// A warp covers WR rows; the tile (one producer stage) covers NCW*WR rows.
+#ifndef SK_XPOL
+#define SK_XPOL 0
+#endif
+#ifndef SK_YPOL
+#define SK_YPOL 0
+#endif
+constexpr bool kXHint = SK_XPOL != 0;  // x gathers marked evict_last in L2
+constexpr bool kYHint = SK_YPOL != 0;  // y / z stores marked evict_first in L2
+
+template <class T, int W>
+struct RPlan {
+    static constexpr int E = int(sizeof(T));
+    static constexpr int VEC = (32 / E) < W ? (32 / E) : W;
+    static constexpr int TPR = W / VEC;   // lanes per row
+    static constexpr int WR = 32 / TPR;   // rows per warp
+    static constexpr bool ok = TPR >= 1 && TPR <= 8 && W % VEC == 0 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0;
+};
+
+template <class T, int C, int W, int U, bool DOTS>
+__global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles,
+                                                                           int seg) {
+    using O = Ops<T>;
+    using P = RPlan<T, W>;
+    constexpr int VEC = P::VEC, TPR = P::TPR, WR = P::WR;
+    constexpr int SCAP = TmaGeom<T, W>::SCAP;
+    constexpr int SB = TmaGeom<T, W>::SB;
+    static_assert(32 % C == 0, "chunk height must divide the warp");
+    auto tile_of = [&](int it, int sg) -> gidx {
+        const gidx q = it / sg, w = it % sg;
+        return (q * gridDim.x + blockIdx.x) * sg + w;
+    };
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ T red[kNCW][3][W];
+    StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + kStages * SB);
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(hdr + kStages);
+    std::uint64_t* empty = full + kStages;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kNCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int chunks_per_tile = rgt * (32 / C);
+    const int rows_per_tile = rgt * 32;
+    constexpr bool want_dots = DOTS;  // launch selects DOTS == (flags & kFlagDots) != 0
+
+    if (warp == kNCW) {
+        // ------------------------------------------------- producer warp (as spmv_tma_kernel)
+        const unsigned long long pol = l2_evict_first_policy();
+        for (int it = 0;; ++it) {
+            const gidx t = tile_of(it, seg);
+            if (t >= ntiles) break;
+            const int s = it % kStages;
+            const std::uint32_t k = std::uint32_t(it / kStages);
+            mbar_wait(&empty[s], (k & 1u) ^ 1u);
+            const gidx c0 = a.rg0 * (32 / C) + t * chunks_per_tile;
+            const gidx c1 = min(min(a.nchunks, a.rg1 * (32 / C)), c0 + chunks_per_tile);
+            const int nc = int(c1 - c0);
+            const gidx off0 = a.chunk_offset[c0];
+            for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
+            for (int q = lane; q < nc; q += 32) hdr[s].hlen[q] = a.chunk_len[c0 + q];
+            const gidx nslots = a.chunk_offset[c1] - off0;
+            const bool fits = nslots <= SCAP;
+            if (lane == 0) {
+                hdr[s].overflow = fits ? 0 : 1;
+                hdr[s].nchunks = nc;
+                hdr[s].off0 = off0;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (fits && nslots > 0) {
+                    T* sval = reinterpret_cast<T*>(smem + s * SB);
+                    lidx* scol = reinterpret_cast<lidx*>(smem + s * SB + SCAP * sizeof(T));
+                    const std::uint32_t vb = std::uint32_t(nslots * sizeof(T));
+                    const std::uint32_t cb = std::uint32_t(nslots * sizeof(lidx));
+                    mbar_arrive_expect_tx(&full[s], vb + cb);
+                    bulk_g2s(sval, a.val + off0, vb, &full[s], pol);
+                    bulk_g2s(scol, a.col + off0, cb, &full[s], pol);
+                } else {
+                    mbar_arrive(&full[s]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------- consumer warps
+        const int sub = lane % TPR;
+        const int rl = lane / TPR;
+        const int rr = warp * WR + rl;  // row within the tile
+        const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
+        const unsigned xrs = unsigned(a.x_rs);
+        const T* xb = a.x + sub * VEC;
+        const unsigned long long xpol = kXHint ? l2_evict_last_policy() : 0ull;
+        const unsigned long long ypol = kYHint ? l2_evict_first_policy() : 0ull;
+        T dsum[3][VEC];
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) dsum[s][e] = O::zero();
+        for (int it = 0;; ++it) {
+            const gidx t = seg == 1 ? gidx(it) * gridDim.x + blockIdx.x : tile_of(it, seg);
+            if (t >= ntiles) break;
+            const int s = it % kStages;
+            const std::uint32_t k = std::uint32_t(it / kStages);
+            mbar_wait(&full[s], k & 1u);
+            const StageHdr& h = hdr[s];
+            const gidx row = (a.rg0 + t * rgt) * 32 + rr;
+            const bool warp_active = warp * WR < rows_per_tile && (a.rg0 + t * rgt) * 32 + warp * WR < a.nrows_padded &&
+                                     (a.rg0 + t * rgt) * 32 + warp * WR < a.rg1 * 32;
+            if (!warp_active) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+            }
+            const int cq = rr / C;
+            const int ip = rr % C;
+            const lidx len = cq < h.nchunks ? h.hlen[cq] : 0;
+            const int off = cq < h.nchunks ? h.hoff[cq] + ip : 0;
+            lidx maxlen = len, minlen = len;
+            if constexpr (C < 32 || WR > C) {
+                maxlen = lidx(__reduce_max_sync(0xffffffffu, unsigned(len)));
+                minlen = lidx(__reduce_min_sync(0xffffffffu, unsigned(len)));
+            }
+            T acc[VEC];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] = O::zero();
+            // value/index source: the shared-memory stage (LDS) or, for a tile that
+            // did not fit one stage, global memory; separate code so the common case
+            // compiles to shared-memory loads.
+            auto gather = [&](const T* vbase, const lidx* cbase) {
+                auto body = [&](lidx j0, auto tail) {
+                    constexpr bool TAIL = decltype(tail)::value;
+                    T vv[U];
+                    Vec<T, VEC> xv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const lidx j = j0 + u;
+                        const int slot = (!TAIL || j < len) ? off + j * C : 0;
+                        vv[u] = vbase[slot];
+                        const unsigned c = unsigned(cbase[slot]);
+                        if constexpr (kXHint && VEC * sizeof(T) == 32)
+                            xv[u] = ld_x_hint<T, VEC>(xb + std::size_t(c) * xrs, xpol);
+                        else
+                            xv[u] = ld_x<T, VEC>(xb + std::size_t(c) * xrs);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const bool ok = !TAIL || (j0 + u < len);
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const T sm = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
+                            if constexpr (TAIL) acc[e] = ok ? sm : acc[e];
+                            else acc[e] = sm;
+                        }
+                    }
+                };
+                lidx j0 = 0;
+                for (; j0 + U <= minlen; j0 += U) body(j0, std::false_type{});
+                for (; j0 < maxlen; j0 += U) body(j0, std::true_type{});
+            };
+            if (!h.overflow)
+                gather(reinterpret_cast<const T*>(smem + s * SB), reinterpret_cast<const lidx*>(smem + s * SB + SCAP * sizeof(T)));
+            else
+                gather(a.val + h.off0, a.col + h.off0);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            // fused epilogue (spmv_epilogue.hpp:12-36)
+            if (row < a.nrows && row < a.rg1 * 32) {
+                const bool fin = !deferred(a.defer_mask, row);
+                const int cb = sub * VEC;
+                T* yp = a.y + row * a.y_rs + cb;
+                Vec<T, VEC> xs, yv, out;
+                if (need_x) xs = ld_x<T, VEC>(a.xs + row * a.xs_rs + cb);
+                if (a.flags & kFlagAxpby) yv = ld_vec<T, VEC>(yp);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e)
+                    out.v[e] = apply_epilogue(a, acc[e], need_x ? xs.v[e] : O::zero(),
+                                              (a.flags & kFlagAxpby) ? yv.v[e] : O::zero(), cb + e);
+                if constexpr (kYHint && VEC * sizeof(T) == 32)
+                    st_vec_hint<T, VEC>(yp, out, ypol);
+                else
+                    st_vec<T, VEC>(yp, out);
+                if (fin) {
+                    if (a.flags & kFlagChain) {
+                        T* zp = a.z + row * a.z_rs + cb;
+                        Vec<T, VEC> zv = ld_vec<T, VEC>(zp);
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) zv.v[e] = O::add(O::mul(a.delta, zv.v[e]), O::mul(a.eta, out.v[e]));
+                        if constexpr (kYHint && VEC * sizeof(T) == 32)
+                            st_vec_hint<T, VEC>(zp, zv, ypol);
+                        else
+                            st_vec<T, VEC>(zp, zv);
+                    }
+                    if (want_dots) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            if (a.flags & kFlagDotYY) dsum[0][e] = O::add(dsum[0][e], O::mul(O::conj(out.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXY) dsum[1][e] = O::add(dsum[1][e], O::mul(O::conj(xs.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXX) dsum[2][e] = O::add(dsum[2][e], O::mul(O::conj(xs.v[e]), xs.v[e]));
+                        }
+                    }
+                }
+            }
+        }
+        if (want_dots) {
+#pragma unroll
+            for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) dsum[s][e] = O::add(dsum[s][e], shfl_xor(dsum[s][e], m));
+            if (lane < TPR) {
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) red[warp][s][lane * VEC + e] = dsum[s][e];
+            }
+        }
+    }
+    if (!want_dots) return;
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * W; t += kTmaThreads) {
+        const int s = t / W, c = t % W;
+        T sum = O::zero();
+        for (int w = 0; w < kNCW; ++w) sum = O::add(sum, red[w][s][c]);
+        a.partial[gidx(blockIdx.x) * 3 * W + t] = sum;
+    }
+}
+
 // Generic fallback (spmv.hpp:68-92): any chunk height, any width, any strides.
 // One thread per (stored row, block of GW columns).
 constexpr int kGW = 8;
@@ -759,10 +999,74 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
     return {grid, grid, 0};
 }
 
+#ifndef SK_RUBUDGET
+#define SK_RUBUDGET 88
+#endif
+#ifndef SK_RUBUDGET_DOTS
+#define SK_RUBUDGET_DOTS 40
+#endif
+// Row-contiguous TMA kernel: unroll so that the in-flight value/index/RHS registers
+// of one gather batch stay within a register budget (smaller when the column-dot
+// accumulators are live).  Measured on B200, 400^3 stencil: w = 8 3.31 ms at U = 8
+// vs 3.44 ms at U = 5; with dots U = 3 beats U = 5.
+template <class T, int W, bool DOTS>
+constexpr int rows_unroll() {
+    constexpr int per = RPlan<T, W>::VEC * int(sizeof(T)) / 4 + int(sizeof(T)) / 4 + 1;
+    constexpr int budget = DOTS ? SK_RUBUDGET_DOTS : SK_RUBUDGET;
+    constexpr int u = budget / per;
+    return u < 1 ? 1 : (u > 8 ? 8 : u);
+}
+
+// SELLKIT_TMA_ROWS = 0 | 1 forces the column-slice / row-contiguous consumer mapping;
+// default: row-contiguous from 32-B RHS rows on.
+inline int rows_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("SELLKIT_TMA_ROWS");
+        return e ? std::atoi(e) : -1;
+    }();
+    return mode;
+}
+
+template <class T, int C, int W, bool DOTS>
+LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
+    constexpr int U = rows_unroll<T, W, DOTS>();
+    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS>;
+    static bool attr = [&] {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tma_smem_bytes<T, W>())));
+        return true;
+    }();
+    (void)attr;
+    static int per_sm = [&] {
+        int nb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, tma_smem_bytes<T, W>()));
+        return std::max(nb, 1);
+    }();
+    const gidx ngroups = a.rg1 - a.rg0;
+    const gidx ntiles = (ngroups + rgt - 1) / rgt;
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
+    static const int seg = [] {
+        const char* e = std::getenv("SELLKIT_TMA_SEG");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    kern<<<grid, kTmaThreads, tma_smem_bytes<T, W>(), st>>>(a, rgt, ntiles, seg);
+    return {grid, grid, 0};
+}
+
 template <class T, int C, int W>
 LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lidx max_chunk_len) {
     using P = Plan<T, W>;
     constexpr int U = unroll_of<T, P>();
+    if constexpr (RPlan<T, W>::ok) {
+        const int rm = rows_mode();
+        const bool rows = rm == 1 || (rm != 0 && W * int(sizeof(T)) >= 32);
+        if (rows && kernel_mode() != 1 && a.row_map == nullptr) {
+            const int cap = TmaGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
+            const int rgt = std::min(kNCW * RPlan<T, W>::WR / 32, cap);
+            if (rgt >= 1)
+                return (a.flags & kFlagDots) ? launch_tma_rows<T, C, W, true>(a, rgt, rt, st)
+                                             : launch_tma_rows<T, C, W, false>(a, rgt, rt, st);
+        }
+    }
     if (kernel_mode() != 1 && a.row_map == nullptr) {
         // row groups per tile: as many as fit one stage, at most one per consumer warp (slice)
         const int cap = TmaGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
