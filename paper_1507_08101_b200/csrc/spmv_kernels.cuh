@@ -618,33 +618,91 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
 #ifndef SK_YPOL
 #define SK_YPOL 0
 #endif
+#ifndef SK_RVEC
+#define SK_RVEC 32  // bytes of one RHS row a lane gathers per nonzero
+#endif
 constexpr bool kXHint = SK_XPOL != 0;  // x gathers marked evict_last in L2
 constexpr bool kYHint = SK_YPOL != 0;  // y / z stores marked evict_first in L2
 
 template <class T, int W>
 struct RPlan {
     static constexpr int E = int(sizeof(T));
-    static constexpr int VEC = (32 / E) < W ? (32 / E) : W;
+    static constexpr int VB = SK_RVEC / E > 0 ? SK_RVEC / E : 1;
+    static constexpr int VEC = VB < W ? VB : W;
     static constexpr int TPR = W / VEC;   // lanes per row
     static constexpr int WR = 32 / TPR;   // rows per warp
     static constexpr bool ok = TPR >= 1 && TPR <= 8 && W % VEC == 0 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0;
 };
 
+// Remainder handling of the row-contiguous kernel: 0 = exact-size batch when the
+// row length is warp-uniform, 1 = predicated batch, 2 = predicated loads too.
+#ifndef SK_TAILMODE
+#define SK_TAILMODE 0
+#endif
+
+// f(integral_constant<R>) for the runtime remainder r in [1, RMAX] (r == 0: nothing)
+template <int RMAX, class F>
+__device__ __forceinline__ void tail_dispatch(int r, F& f) {
+    if constexpr (RMAX >= 1) {
+        if (r == RMAX)
+            f(std::integral_constant<int, RMAX>{});
+        else
+            tail_dispatch<RMAX - 1>(r, f);
+    }
+}
+
+// Occupancy of the row-contiguous kernel.  The consumers are latency bound (each
+// warp has one batch of gathers in flight, then computes), so resident warps are
+// worth more than unroll depth or stage depth: measured on B200 (400^3, w = 8),
+// 2 CTAs/SM x 3 stages x U = 8: 3.46 ms; 3 CTAs x 3 x U = 4: 2.55 ms;
+// 4 CTAs x 2 stages x U = 3: 2.47 ms.  The dots variant keeps 3 x VEC extra
+// accumulators live and runs at one CTA less.
+#ifndef SK_RMINB
+#define SK_RMINB 4
+#endif
+#ifndef SK_RMINB_DOTS
+#define SK_RMINB_DOTS 3
+#endif
+#ifndef SK_RSTAGES
+#define SK_RSTAGES 2
+#endif
+#ifndef SK_RSTAGE_KB
+#define SK_RSTAGE_KB 16
+#endif
+#ifndef SK_RSTAGE_KB_NARROW
+#define SK_RSTAGE_KB_NARROW 24
+#endif
+constexpr int kRStages = SK_RSTAGES;
+
+// Stage size: a tile is kNCW * WR rows, so narrow blocks (WR = 32) need deeper
+// stages to give every consumer warp its rows.
+template <class T, int W>
+struct RGeom {
+    static constexpr int SB = (W * int(sizeof(T)) >= 32 ? SK_RSTAGE_KB : SK_RSTAGE_KB_NARROW) * 1024;
+    static constexpr int SCAP = (SB / int(sizeof(T) + 4)) / 32 * 32;  // slots per stage
+};
+
+template <class T, int W>
+constexpr std::size_t rows_smem_bytes() {
+    return std::size_t(kRStages) * RGeom<T, W>::SB + std::size_t(kRStages) * sizeof(StageHdr) + 2 * kRStages * 8 + 128;
+}
+
 template <class T, int C, int W, int U, bool DOTS>
-__global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles,
-                                                                           int seg) {
+__global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
+    spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
     using P = RPlan<T, W>;
     constexpr int VEC = P::VEC, TPR = P::TPR, WR = P::WR;
-    constexpr int SCAP = TmaGeom<T, W>::SCAP;
-    constexpr int SB = TmaGeom<T, W>::SB;
+    constexpr int SCAP = RGeom<T, W>::SCAP;
+    constexpr int SB = RGeom<T, W>::SB;
+    constexpr int kStages = kRStages;
     static_assert(32 % C == 0, "chunk height must divide the warp");
     auto tile_of = [&](int it, int sg) -> gidx {
         const gidx q = it / sg, w = it % sg;
         return (q * gridDim.x + blockIdx.x) * sg + w;
     };
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ T red[kNCW][3][W];
+    __shared__ T red[DOTS ? kNCW : 1][3][DOTS ? W : 1];
     StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + kStages * SB);
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(hdr + kStages);
     std::uint64_t* empty = full + kStages;
@@ -744,36 +802,83 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_rows_kernel(con
             // value/index source: the shared-memory stage (LDS) or, for a tile that
             // did not fit one stage, global memory; separate code so the common case
             // compiles to shared-memory loads.
-            auto gather = [&](const T* vbase, const lidx* cbase) {
-                auto body = [&](lidx j0, auto tail) {
-                    constexpr bool TAIL = decltype(tail)::value;
-                    T vv[U];
-                    Vec<T, VEC> xv[U];
+            // RHS row c starts at byte xbytes + c * xstride (one IMAD.WIDE per gather)
+            const char* xbytes = reinterpret_cast<const char*>(xb);
+            const unsigned xstride = xrs * unsigned(sizeof(T));
+            auto gather = [&](const T* vp, const lidx* cp) {
+                // slot (row, j) = off + j*C: walk the per-lane pointers by U*C per batch,
+                // so the U slots of a batch are immediate offsets
+                vp += off;
+                cp += off;
+                auto xrow = [&](lidx c) -> const T* {
+                    return reinterpret_cast<const T*>(xbytes + (unsigned long long)unsigned(c) * xstride);
+                };
+                auto ldx = [&](const T* p) -> Vec<T, VEC> {
+                    if constexpr (kXHint && VEC * sizeof(T) == 32) return ld_x_hint<T, VEC>(p, xpol);
+                    else return ld_x<T, VEC>(p);
+                };
+                // one batch of R consecutive j: all loads first, then the products in j order
+                auto batch = [&](auto rc) {
+                    constexpr int R = decltype(rc)::value;
+                    T vv[R];
+                    Vec<T, VEC> xv[R];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const lidx j = j0 + u;
-                        const int slot = (!TAIL || j < len) ? off + j * C : 0;
-                        vv[u] = vbase[slot];
-                        const unsigned c = unsigned(cbase[slot]);
-                        if constexpr (kXHint && VEC * sizeof(T) == 32)
-                            xv[u] = ld_x_hint<T, VEC>(xb + std::size_t(c) * xrs, xpol);
-                        else
-                            xv[u] = ld_x<T, VEC>(xb + std::size_t(c) * xrs);
+                    for (int u = 0; u < R; ++u) {
+                        vv[u] = vp[u * C];
+                        xv[u] = ldx(xrow(cp[u * C]));
                     }
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const bool ok = !TAIL || (j0 + u < len);
+                    for (int u = 0; u < R; ++u)
 #pragma unroll
-                        for (int e = 0; e < VEC; ++e) {
-                            const T sm = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
-                            if constexpr (TAIL) acc[e] = ok ? sm : acc[e];
-                            else acc[e] = sm;
-                        }
-                    }
+                        for (int e = 0; e < VEC; ++e) acc[e] = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
+                    vp += R * C;
+                    cp += R * C;
                 };
                 lidx j0 = 0;
-                for (; j0 + U <= minlen; j0 += U) body(j0, std::false_type{});
-                for (; j0 < maxlen; j0 += U) body(j0, std::true_type{});
+                for (; j0 + U <= minlen; j0 += U) batch(std::integral_constant<int, U>{});
+                if (SK_TAILMODE == 0 && minlen == maxlen) {
+                    // warp-uniform row length (every row of the warp in one chunk, the usual
+                    // case): the remainder is one exact-size batch, no predicates
+                    tail_dispatch<U - 1>(len - j0, batch);
+                } else {
+                    // rows of different chunks: predicated adds; out-of-row slots gather RHS
+                    // row 0 (always valid) and their products are dropped, so the sum is the
+                    // reference's exactly
+                    for (; j0 < maxlen; j0 += U) {
+                        T vv[U];
+                        Vec<T, VEC> xv[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const bool ok = j0 + u < len;
+                            if constexpr (SK_TAILMODE == 2) {
+#pragma unroll
+                                for (int e = 0; e < VEC; ++e) xv[u].v[e] = O::zero();
+                                vv[u] = O::zero();
+                                if (ok) {
+                                    vv[u] = vp[u * C];
+                                    xv[u] = ldx(xrow(cp[u * C]));
+                                }
+                            } else {
+                                lidx c = 0;
+                                vv[u] = O::zero();
+                                if (ok) {
+                                    c = cp[u * C];
+                                    vv[u] = vp[u * C];
+                                }
+                                xv[u] = ldx(xrow(c));
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (j0 + u < len) {
+#pragma unroll
+                                for (int e = 0; e < VEC; ++e) acc[e] = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
+                            }
+                        }
+                        vp += U * C;
+                        cp += U * C;
+                    }
+                }
             };
             if (!h.overflow)
                 gather(reinterpret_cast<const T*>(smem + s * SB), reinterpret_cast<const lidx*>(smem + s * SB + SCAP * sizeof(T)));
@@ -1000,15 +1105,14 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
 }
 
 #ifndef SK_RUBUDGET
-#define SK_RUBUDGET 88
+#define SK_RUBUDGET 33
 #endif
 #ifndef SK_RUBUDGET_DOTS
-#define SK_RUBUDGET_DOTS 40
+#define SK_RUBUDGET_DOTS 22
 #endif
 // Row-contiguous TMA kernel: unroll so that the in-flight value/index/RHS registers
-// of one gather batch stay within a register budget (smaller when the column-dot
-// accumulators are live).  Measured on B200, 400^3 stencil: w = 8 3.31 ms at U = 8
-// vs 3.44 ms at U = 5; with dots U = 3 beats U = 5.
+// of one gather batch stay within a register budget that fits the occupancy
+// target (SK_RMINB CTAs/SM: 56 registers per thread at 4).
 template <class T, int W, bool DOTS>
 constexpr int rows_unroll() {
     constexpr int per = RPlan<T, W>::VEC * int(sizeof(T)) / 4 + int(sizeof(T)) / 4 + 1;
@@ -1031,14 +1135,15 @@ template <class T, int C, int W, bool DOTS>
 LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS>;
+    constexpr std::size_t smem = rows_smem_bytes<T, W>();
     static bool attr = [&] {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tma_smem_bytes<T, W>())));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         return true;
     }();
     (void)attr;
     static int per_sm = [&] {
         int nb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, tma_smem_bytes<T, W>()));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, smem));
         return std::max(nb, 1);
     }();
     const gidx ngroups = a.rg1 - a.rg0;
@@ -1048,7 +1153,7 @@ LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaS
         const char* e = std::getenv("SELLKIT_TMA_SEG");
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
-    kern<<<grid, kTmaThreads, tma_smem_bytes<T, W>(), st>>>(a, rgt, ntiles, seg);
+    kern<<<grid, kTmaThreads, smem, st>>>(a, rgt, ntiles, seg);
     return {grid, grid, 0};
 }
 
@@ -1058,9 +1163,10 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
     constexpr int U = unroll_of<T, P>();
     if constexpr (RPlan<T, W>::ok) {
         const int rm = rows_mode();
-        const bool rows = rm == 1 || (rm != 0 && W * int(sizeof(T)) >= 32);
-        if (rows && kernel_mode() != 1 && a.row_map == nullptr) {
-            const int cap = TmaGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
+        const bool rows = rm != 0;
+        const bool stride_ok = gidx(a.x_rs) * gidx(sizeof(T)) < (gidx(1) << 31);  // 32-bit byte stride
+        if (rows && stride_ok && kernel_mode() != 1 && a.row_map == nullptr) {
+            const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
             const int rgt = std::min(kNCW * RPlan<T, W>::WR / 32, cap);
             if (rgt >= 1)
                 return (a.flags & kFlagDots) ? launch_tma_rows<T, C, W, true>(a, rgt, rt, st)
