@@ -682,9 +682,16 @@ struct RGeom {
     static constexpr int SCAP = (SB / int(sizeof(T) + 4)) / 32 * 32;  // slots per stage
 };
 
+// stage ring, headers, barriers; with dots also the per-lane dot accumulators
+// dacc[3][VEC][consumer lanes] (lane-contiguous: conflict-free)
 template <class T, int W>
+constexpr std::size_t rows_stage_bytes() {
+    return (std::size_t(kRStages) * RGeom<T, W>::SB + std::size_t(kRStages) * sizeof(StageHdr) + 2 * kRStages * 8 + 15) /
+           16 * 16;
+}
+template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
-    return std::size_t(kRStages) * RGeom<T, W>::SB + std::size_t(kRStages) * sizeof(StageHdr) + 2 * kRStages * 8 + 128;
+    return rows_stage_bytes<T, W>() + (DOTS ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) + 128;
 }
 
 template <class T, int C, int W, int U, bool DOTS>
@@ -767,11 +774,16 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
         const T* xb = a.x + sub * VEC;
         const unsigned long long xpol = kXHint ? l2_evict_last_policy() : 0ull;
         const unsigned long long ypol = kYHint ? l2_evict_first_policy() : 0ull;
-        T dsum[3][VEC];
+        // column dots: every lane accumulates its rows' terms in its own shared-memory
+        // slots (no 3 x VEC accumulators live across the gather loop); the lanes are
+        // reduced once at the end, in a fixed order (deterministic)
+        T* dacc = reinterpret_cast<T*>(smem + rows_stage_bytes<T, W>());
+        const int cl = warp * 32 + lane;  // consumer lane
+        constexpr int NCL = kNCW * 32;
+        if constexpr (DOTS) {
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) dsum[s][e] = O::zero();
+            for (int q = 0; q < 3 * VEC; ++q) dacc[q * NCL + cl] = O::zero();
+        }
         for (int it = 0;; ++it) {
             const gidx t = seg == 1 ? gidx(it) * gridDim.x + blockIdx.x : tile_of(it, seg);
             if (t >= ntiles) break;
@@ -913,29 +925,31 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                         else
                             st_vec<T, VEC>(zp, zv);
                     }
-                    if (want_dots) {
+                    if constexpr (DOTS) {
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) {
-                            if (a.flags & kFlagDotYY) dsum[0][e] = O::add(dsum[0][e], O::mul(O::conj(out.v[e]), out.v[e]));
-                            if (a.flags & kFlagDotXY) dsum[1][e] = O::add(dsum[1][e], O::mul(O::conj(xs.v[e]), out.v[e]));
-                            if (a.flags & kFlagDotXX) dsum[2][e] = O::add(dsum[2][e], O::mul(O::conj(xs.v[e]), xs.v[e]));
+                            T* dp = dacc + e * NCL + cl;
+                            if (a.flags & kFlagDotYY) dp[0] = O::add(dp[0], O::mul(O::conj(out.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXY)
+                                dp[VEC * NCL] = O::add(dp[VEC * NCL], O::mul(O::conj(xs.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXX)
+                                dp[2 * VEC * NCL] = O::add(dp[2 * VEC * NCL], O::mul(O::conj(xs.v[e]), xs.v[e]));
                         }
                     }
                 }
             }
         }
-        if (want_dots) {
+        if constexpr (DOTS) {
+            // lanes of a row slot -> warp total per column (fixed butterfly order)
 #pragma unroll
-            for (int m = TPR; m < 32; m <<= 1)
+            for (int q = 0; q < 3; ++q) {
 #pragma unroll
-                for (int s = 0; s < 3; ++s)
+                for (int e = 0; e < VEC; ++e) {
+                    T v = dacc[(q * VEC + e) * NCL + cl];
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) dsum[s][e] = O::add(dsum[s][e], shfl_xor(dsum[s][e], m));
-            if (lane < TPR) {
-#pragma unroll
-                for (int s = 0; s < 3; ++s)
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) red[warp][s][lane * VEC + e] = dsum[s][e];
+                    for (int m = TPR; m < 32; m <<= 1) v = O::add(v, shfl_xor(v, m));
+                    if (lane < TPR) red[warp][q][lane * VEC + e] = v;
+                }
             }
         }
     }
@@ -1108,7 +1122,7 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
 #define SK_RUBUDGET 33
 #endif
 #ifndef SK_RUBUDGET_DOTS
-#define SK_RUBUDGET_DOTS 22
+#define SK_RUBUDGET_DOTS 44
 #endif
 // Row-contiguous TMA kernel: unroll so that the in-flight value/index/RHS registers
 // of one gather batch stay within a register budget that fits the occupancy
@@ -1135,7 +1149,7 @@ template <class T, int C, int W, bool DOTS>
 LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS>;
-    constexpr std::size_t smem = rows_smem_bytes<T, W>();
+    constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
     static bool attr = [&] {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         return true;
