@@ -30,6 +30,44 @@ i64 = C.c_int64
 i32 = C.c_int32
 
 
+class RefIO:
+    """The reference's own file readers/writers (oracle/_ref/libsellkit.so, built
+    from /root/reference/proj/src by oracle/Makefile.ref), bound through its C ABI
+    (proj/include/sellkit.h:84-87).  Used as the parity checker for the I/O path:
+    ``mm_to_gcrs`` / ``gcrs_to_gcrs`` return the reference's GCRS bytes, or the
+    reference's error code (an int) when it rejects the file."""
+
+    def __init__(self, path: str = REF_LIB_PATH):
+        lib = C.CDLL(path)
+        lib.sellkit_crs_read_mm.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
+        lib.sellkit_crs_read_mm.restype = C.c_int
+        lib.sellkit_crs_read_bin.argtypes = [C.c_char_p, C.POINTER(vp)]
+        lib.sellkit_crs_read_bin.restype = C.c_int
+        lib.sellkit_crs_write_bin.argtypes = [C.c_char_p, vp, C.c_int]
+        lib.sellkit_crs_write_bin.restype = C.c_int
+        lib.sellkit_crs_destroy.argtypes = [vp]
+        lib.sellkit_crs_destroy.restype = None
+        self.lib = lib
+
+    def _write(self, h, out_path: str, wide: bool):
+        err = self.lib.sellkit_crs_write_bin(os.fsencode(out_path), h, 1 if wide else 0)
+        self.lib.sellkit_crs_destroy(h)
+        if err:
+            return err
+        with open(out_path, "rb") as f:
+            return f.read()
+
+    def mm_to_gcrs(self, mm_path: str, dt: int, out_path: str, wide: bool = False):
+        h = vp()
+        err = self.lib.sellkit_crs_read_mm(os.fsencode(mm_path), dt, C.byref(h))
+        return err if err else self._write(h, out_path, wide)
+
+    def gcrs_to_gcrs(self, in_path: str, out_path: str, wide: bool = False):
+        h = vp()
+        err = self.lib.sellkit_crs_read_bin(os.fsencode(in_path), C.byref(h))
+        return err if err else self._write(h, out_path, wide)
+
+
 class OrSell(C.Structure):
     _fields_ = [("nrows", i32), ("ncols", i32), ("nrows_padded", i32), ("C", i32), ("sigma", i32),
                 ("cols_permuted", i32), ("dt", i32), ("nnz", i64), ("nchunks", i64), ("slots", i64),

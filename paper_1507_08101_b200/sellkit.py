@@ -234,6 +234,18 @@ class Sellkit:
         self.call("sellkit_crs_create", dt, nrows, ncols, _ptr(rowptr), _ptr(col), _ptr(val), C.byref(out))
         return Crs(self, out, dt)
 
+    def crs_read_mm(self, path: str, dt=R64) -> "Crs":
+        """Matrix Market file -> device CRS (reference io.cpp:206-301)."""
+        out = vp()
+        self.call("sellkit_crs_read_mm", os.fsencode(path), dt, C.byref(out))
+        return Crs(self, out, dt)
+
+    def crs_read_bin(self, path: str) -> "Crs":
+        """GCRS binary file -> device CRS; the element type comes from the header (io.cpp:303-333)."""
+        out = vp()
+        self.call("sellkit_crs_read_bin", os.fsencode(path), C.byref(out))
+        return Crs(self, out, self.lib.sellkit_crs_datatype(out))
+
     def crs_stencil(self, points: int, n: int, row_begin: int = 0, row_end: Optional[int] = None, dt=R64) -> "Crs":
         N = n * n if points == 5 else n ** 3
         out = vp()
@@ -338,6 +350,9 @@ class Crs(_Handle):
         out = vp()
         self.sk.call("sellkit_mat_build", self.h, chunk_height, sigma, C.byref(out))
         return Mat(self.sk, out, self.dt)
+
+    def write_bin(self, path: str, wide_cols: bool = False):
+        self.sk.call("sellkit_crs_write_bin", os.fsencode(path), self.h, 1 if wide_cols else 0)
 
 
 class Mat(_Handle):
