@@ -224,6 +224,18 @@ __device__ __forceinline__ Vec<T, N> ld_x_hint(const T* p, unsigned long long po
 }
 
 template <class T, int N>
+__device__ __forceinline__ Vec<T, N> ld_vec_hint(const T* p, unsigned long long pol) {
+    static_assert(int(sizeof(T)) * N == 32, "32-byte loads only");
+    Vec<T, N> r;
+    unsigned long long t[4];
+    asm volatile("ld.global.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(t[0]), "=l"(t[1]), "=l"(t[2]), "=l"(t[3])
+                 : "l"(p), "l"(pol));
+    memcpy(&r, t, 32);
+    return r;
+}
+
+template <class T, int N>
 __device__ __forceinline__ void st_vec_hint(T* p, const Vec<T, N>& v, unsigned long long pol) {
     static_assert(int(sizeof(T)) * N == 32, "32-byte stores only");
     unsigned long long t[4];

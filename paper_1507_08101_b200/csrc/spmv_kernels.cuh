@@ -621,6 +621,10 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
 #ifndef SK_RVEC
 #define SK_RVEC 32  // bytes of one RHS row a lane gathers per nonzero
 #endif
+#ifndef SK_PREFETCH_EPI
+#define SK_PREFETCH_EPI 1
+#endif
+constexpr bool kPrefetchEpi = SK_PREFETCH_EPI != 0;
 constexpr bool kXHint = SK_XPOL != 0;  // x gathers marked evict_last in L2
 constexpr bool kYHint = SK_YPOL != 0;  // y / z stores marked evict_first in L2
 
@@ -735,6 +739,23 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             if (t >= ntiles) break;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
+            // the epilogue's y (AXPBY) and z (CHAIN) rows of this tile: one bulk L2
+            // prefetch each, a stage ahead of the consumers, so the epilogue reads
+            // hit L2 instead of adding a dependent HBM round trip per tile
+            if (kPrefetchEpi && lane == 0 && (a.flags & (kFlagAxpby | kFlagChain))) {
+                const gidx r0 = (a.rg0 + t * rgt) * 32;
+                const gidx r1 = min(r0 + gidx(rows_per_tile), min(gidx(a.nrows), a.rg1 * 32));
+                auto span = [&](const T* base, gidx rs) {
+                    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(base + r0 * rs) & ~std::uintptr_t(15);
+                    const std::uintptr_t e =
+                        (reinterpret_cast<std::uintptr_t>(base + (r1 - 1) * rs + W) + 15) & ~std::uintptr_t(15);
+                    bulk_prefetch_l2(reinterpret_cast<const void*>(b), std::uint32_t(e - b));
+                };
+                if (r1 > r0) {
+                    if (a.flags & kFlagAxpby) span(a.y, a.y_rs);
+                    if (a.flags & kFlagChain) span(a.z, a.z_rs);
+                }
+            }
             mbar_wait(&empty[s], (k & 1u) ^ 1u);
             const gidx c0 = a.rg0 * (32 / C) + t * chunks_per_tile;
             const gidx c1 = min(min(a.nchunks, a.rg1 * (32 / C)), c0 + chunks_per_tile);
@@ -789,9 +810,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             if (t >= ntiles) break;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
+            const gidx row = (a.rg0 + t * rgt) * 32 + rr;
             mbar_wait(&full[s], k & 1u);
             const StageHdr& h = hdr[s];
-            const gidx row = (a.rg0 + t * rgt) * 32 + rr;
             const bool warp_active = warp * WR < rows_per_tile && (a.rg0 + t * rgt) * 32 + warp * WR < a.nrows_padded &&
                                      (a.rg0 + t * rgt) * 32 + warp * WR < a.rg1 * 32;
             if (!warp_active) {
@@ -905,7 +926,12 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 T* yp = a.y + row * a.y_rs + cb;
                 Vec<T, VEC> xs, yv, out;
                 if (need_x) xs = ld_x<T, VEC>(a.xs + row * a.xs_rs + cb);
-                if (a.flags & kFlagAxpby) yv = ld_vec<T, VEC>(yp);
+                if (a.flags & kFlagAxpby) {
+                    if constexpr (kYHint && VEC * sizeof(T) == 32)
+                        yv = ld_vec_hint<T, VEC>(yp, ypol);
+                    else
+                        yv = ld_vec<T, VEC>(yp);
+                }
 #pragma unroll
                 for (int e = 0; e < VEC; ++e)
                     out.v[e] = apply_epilogue(a, acc[e], need_x ? xs.v[e] : O::zero(),
