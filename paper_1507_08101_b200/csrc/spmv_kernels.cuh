@@ -749,7 +749,10 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                     const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(base + r0 * rs) & ~std::uintptr_t(15);
                     const std::uintptr_t e =
                         (reinterpret_cast<std::uintptr_t>(base + (r1 - 1) * rs + W) + 15) & ~std::uintptr_t(15);
-                    bulk_prefetch_l2(reinterpret_cast<const void*>(b), std::uint32_t(e - b));
+                    if constexpr (kYHint)
+                        bulk_prefetch_l2(reinterpret_cast<const void*>(b), std::uint32_t(e - b), pol);
+                    else
+                        bulk_prefetch_l2(reinterpret_cast<const void*>(b), std::uint32_t(e - b));
                 };
                 if (r1 > r0) {
                     if (a.flags & kFlagAxpby) span(a.y, a.y_rs);

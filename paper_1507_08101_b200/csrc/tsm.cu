@@ -457,6 +457,15 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
                 const T* vp = reinterpret_cast<const T*>(vs.dev.data);
                 const T* wp = reinterpret_cast<const T*>(wsg.dev.data);
                 const gidx vst = vs.dev.stride, wst = wsg.dev.stride;
+                int used = 0;
+                if constexpr (std::is_same_v<T, double>) {
+                    if (!kahan && cells > 64 && vst == m && wst == k)
+                        used = tsmttsm_dmma_partials(vp, wp, n, m, k, p, nparts, rt);
+                }
+                if (used > 0) {
+                    tsmttsm_final_kernel<T, false><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, used, m, k, xa, a, b);
+                    return 0;
+                }
                 if (m <= 8 && k <= 8) {
                     auto go = [&]<int MM, int KK>() {
                         if (kahan) tsmttsm_reg_kernel<T, MM, KK, true><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
@@ -573,6 +582,9 @@ void tsmm(DenseMat& w, const DenseMat& v_in, const DenseMat& x_in, const void* a
                 T* wp = reinterpret_cast<T*>(wsg.dev.data);
                 const T* vp = reinterpret_cast<const T*>(vs.dev.data);
                 const gidx wst = wsg.dev.stride, vst = vs.dev.stride;
+                if constexpr (std::is_same_v<T, double>) {
+                    if (!exact && vst == m && wst == k && tsmm_dmma(wp, vp, xc, n, m, k, a, b, beta_zero, rt)) return 0;
+                }
                 auto go = [&]<int RT, int KT, bool EX>() {
                     auto kern = tsmm_tile_kernel<T, RT, KT, EX>;
                     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(xbytes)));
