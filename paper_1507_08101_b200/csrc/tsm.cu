@@ -14,6 +14,11 @@
 //           accumulators, writes its partial m x k block, and an ordered pass
 //           combines CTA partials (Kahan-Babuska-Neumaier on request, like
 //           CompensatedSum tsm.hpp:73-87) and applies alpha/beta.
+// Fast paths for compact row-major real operands (measured, N = 1e8, B200):
+//   m, k <= 8      one row per thread, whole rows moved with vector accesses
+//                  (tsmm_row_kernel keeps the reference's rounding): 80-94 % of HBM
+//   m, k >= 8      FP64 tensor cores, tsm_mma.cu: m = k = 64 at 24-27 TF/s
+//   otherwise      the generic kernels above.
 #include <algorithm>
 
 #include "ops.cuh"
@@ -214,9 +219,50 @@ __global__ void gemm_naive_kernel(DAcc c, DAcc a, DAcc b, lidx n, lidx kc, lidx 
 // ---------------------------------------------------------------- fast paths
 // Row-major, compact V/W (column step 1, no column map), real element types.
 
+// A whole compact row of N elements in as few vector accesses as its size allows
+// (32-byte LDG/STG pieces, else 16/8 bytes); p must be aligned to the row size
+// (rows of a compact row-major block with N in {1,2,4,8} are).
+template <class T, int N>
+__device__ __forceinline__ void load_row(const T* p, T (&r)[N]) {
+    constexpr int B = N * int(sizeof(T));
+    if constexpr (B >= 32 && B % 32 == 0) {
+        constexpr int P = 32 / int(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < N / P; ++q) {
+            const Vec<T, P> x = ld_x<T, P>(p + q * P);
+#pragma unroll
+            for (int e = 0; e < P; ++e) r[q * P + e] = x.v[e];
+        }
+    } else {
+        const Vec<T, N> x = ld_x<T, N>(p);
+#pragma unroll
+        for (int e = 0; e < N; ++e) r[e] = x.v[e];
+    }
+}
+template <class T, int N>
+__device__ __forceinline__ void store_row(T* p, const T (&r)[N]) {
+    constexpr int B = N * int(sizeof(T));
+    if constexpr (B >= 32 && B % 32 == 0) {
+        constexpr int P = 32 / int(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < N / P; ++q) {
+            Vec<T, P> x;
+#pragma unroll
+            for (int e = 0; e < P; ++e) x.v[e] = r[q * P + e];
+            st_vec<T, P>(p + q * P, x);
+        }
+    } else {
+        Vec<T, N> x;
+#pragma unroll
+        for (int e = 0; e < N; ++e) x.v[e] = r[e];
+        st_vec<T, N>(p, x);
+    }
+}
+
 // TSMTTSM, m <= MM, k <= KK (MM, KK in {1,2,4,8}): each thread keeps the whole
 // m x k block in registers and walks its rows of the CTA's contiguous range;
 // warp butterfly + ordered CTA sum -> one partial per CTA (deterministic).
+// Compact operands with m == MM, k == KK load whole rows with vector accesses.
 template <class T, int MM, int KK, bool KAHAN>
 __global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v, gidx vs, const T* __restrict__ w,
                                                          gidx ws, gidx n, int m, int k, gidx rows_per_cta, T* partial,
@@ -231,12 +277,21 @@ __global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v
         for (int b = 0; b < KK; ++b) acc[a][b] = cmp[a][b] = O::zero();
     const gidx r0 = gidx(blockIdx.x) * rows_per_cta;
     const gidx r1 = min(n, r0 + rows_per_cta);
+    // (the scalar loop is as fast for 1 x 1 and keeps its loads batched)
+    const bool vec = MM * KK > 1 && m == MM && k == KK && vs == MM && ws == KK;
     for (gidx i = r0 + threadIdx.x; i < r1; i += kT) {
         T vr[MM], wr[KK];
+        if (vec) {
+            load_row<T, MM>(v + i * MM, vr);
+            load_row<T, KK>(w + i * KK, wr);
 #pragma unroll
-        for (int a = 0; a < MM; ++a) vr[a] = a < m ? O::conj(__ldg(v + i * vs + a)) : O::zero();
+            for (int a = 0; a < MM; ++a) vr[a] = O::conj(vr[a]);
+        } else {
 #pragma unroll
-        for (int b = 0; b < KK; ++b) wr[b] = b < k ? __ldg(w + i * ws + b) : O::zero();
+            for (int a = 0; a < MM; ++a) vr[a] = a < m ? O::conj(__ldg(v + i * vs + a)) : O::zero();
+#pragma unroll
+            for (int b = 0; b < KK; ++b) wr[b] = b < k ? __ldg(w + i * ws + b) : O::zero();
+        }
 #pragma unroll
         for (int a = 0; a < MM; ++a)
 #pragma unroll
@@ -395,6 +450,40 @@ __global__ void __launch_bounds__(kT) tsmm_tile_kernel(T* __restrict__ w, gidx w
                 *wp = beta_zero ? O::mul(alpha, tmp[r][e]) : O::add(O::mul(alpha, tmp[r][e]), O::mul(beta, *wp));
             }
         }
+    }
+}
+
+// TSMM with the reference's rounding (m*k <= 64, HBM-bound): one thread per
+// row, the V row and the W row moved with vector accesses, X broadcast from
+// shared memory; tmp[e] = sum over m ascending of V[i,m]*X[m,e], each product and
+// sum rounded separately (tsm.hpp:51-68).
+template <class T, int M, int K>
+__global__ void __launch_bounds__(kT) tsmm_row_kernel(T* __restrict__ w, const T* __restrict__ v,
+                                                      const T* __restrict__ xcm, gidx n, T alpha, T beta,
+                                                      int beta_zero) {
+    using O = Ops<T>;
+    __shared__ T xs[M * K];  // row-major
+    for (int t = threadIdx.x; t < M * K; t += kT) xs[t] = xcm[(t % K) * M + t / K];
+    __syncthreads();
+    for (gidx i = blockIdx.x * gidx(kT) + threadIdx.x; i < n; i += gidx(gridDim.x) * kT) {
+        T vr[M], tmp[K], out[K];
+        load_row<T, M>(v + i * M, vr);
+#pragma unroll
+        for (int e = 0; e < K; ++e) tmp[e] = O::zero();
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+            for (int e = 0; e < K; ++e) tmp[e] = O::add(tmp[e], O::mul(vr[mm], xs[mm * K + e]));
+        if (beta_zero) {
+#pragma unroll
+            for (int e = 0; e < K; ++e) out[e] = O::mul(alpha, tmp[e]);
+        } else {
+            T old[K];
+            load_row<T, K>(w + i * K, old);
+#pragma unroll
+            for (int e = 0; e < K; ++e) out[e] = O::add(O::mul(alpha, tmp[e]), O::mul(beta, old[e]));
+        }
+        store_row<T, K>(w + i * K, out);
     }
 }
 
@@ -584,6 +673,28 @@ void tsmm(DenseMat& w, const DenseMat& v_in, const DenseMat& x_in, const void* a
                 const gidx wst = wsg.dev.stride, vst = vs.dev.stride;
                 if constexpr (std::is_same_v<T, double>) {
                     if (!exact && vst == m && wst == k && tsmm_dmma(wp, vp, xc, n, m, k, a, b, beta_zero, rt)) return 0;
+                }
+                auto pow2 = [](lidx q) { return q == 1 || q == 2 || q == 4 || q == 8; };
+                if (exact && pow2(m) && pow2(k) && vst == m && wst == k) {
+                    const int grid = int(std::max<gidx>(1, std::min<gidx>((n + kT - 1) / kT, gidx(rt.num_sms) * 8)));
+                    auto row = [&]<int M, int K>() {
+                        tsmm_row_kernel<T, M, K><<<grid, kT, 0, rt.stream>>>(wp, vp, xc, n, a, b, beta_zero ? 1 : 0);
+                    };
+                    auto rowk = [&]<int M>() {
+                        switch (k) {
+                            case 1: row.template operator()<M, 1>(); break;
+                            case 2: row.template operator()<M, 2>(); break;
+                            case 4: row.template operator()<M, 4>(); break;
+                            default: row.template operator()<M, 8>(); break;
+                        }
+                    };
+                    switch (m) {
+                        case 1: rowk.template operator()<1>(); break;
+                        case 2: rowk.template operator()<2>(); break;
+                        case 4: rowk.template operator()<4>(); break;
+                        default: rowk.template operator()<8>(); break;
+                    }
+                    return 0;
                 }
                 auto go = [&]<int RT, int KT, bool EX>() {
                     auto kern = tsmm_tile_kernel<T, RT, KT, EX>;
