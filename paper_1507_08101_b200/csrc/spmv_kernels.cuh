@@ -698,7 +698,7 @@ constexpr std::size_t rows_smem_bytes() {
     return rows_stage_bytes<T, W>() + (DOTS ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) + 128;
 }
 
-template <class T, int C, int W, int U, bool DOTS>
+template <class T, int C, int W, int U, bool DOTS, bool PLAIN>
 __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
     spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
@@ -922,6 +922,16 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 gather(a.val + h.off0, a.col + h.off0);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if constexpr (PLAIN) {
+                // y = A x with alpha == 1 and no other flag: t * 1 == t, so the store is the result
+                if (row < a.nrows && row < a.rg1 * 32) {
+                    Vec<T, VEC> out;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) out.v[e] = acc[e];
+                    st_vec<T, VEC>(a.y + row * a.y_rs + sub * VEC, out);
+                }
+                continue;
+            }
             // fused epilogue (spmv_epilogue.hpp:12-36)
             if (row < a.nrows && row < a.rg1 * 32) {
                 const bool fin = !deferred(a.defer_mask, row);
@@ -1174,10 +1184,10 @@ inline int rows_mode() {
     return mode;
 }
 
-template <class T, int C, int W, bool DOTS>
+template <class T, int C, int W, bool DOTS, bool PLAIN>
 LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     constexpr int U = rows_unroll<T, W, DOTS>();
-    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS>;
+    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
     static bool attr = [&] {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1211,9 +1221,16 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
         if (rows && stride_ok && kernel_mode() != 1 && a.row_map == nullptr) {
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
             const int rgt = std::min(kNCW * RPlan<T, W>::WR / 32, cap);
-            if (rgt >= 1)
-                return (a.flags & kFlagDots) ? launch_tma_rows<T, C, W, true>(a, rgt, rt, st)
-                                             : launch_tma_rows<T, C, W, false>(a, rgt, rt, st);
+            if (rgt >= 1) {
+                if (a.flags & kFlagDots) return launch_tma_rows<T, C, W, true, false>(a, rgt, rt, st);
+                // plain y = A x: no flag, alpha == 1, no deferred rows
+                const T one = Ops<T>::one();
+                static const bool no_plain = std::getenv("SELLKIT_SPMV_NOPLAIN") != nullptr;  // A/B switch
+                const bool plain = !no_plain && a.flags == 0 && a.defer_mask == nullptr &&
+                                   std::memcmp(&a.alpha, &one, sizeof(T)) == 0;
+                return plain ? launch_tma_rows<T, C, W, false, true>(a, rgt, rt, st)
+                             : launch_tma_rows<T, C, W, false, false>(a, rgt, rt, st);
+            }
         }
     }
     if (kernel_mode() != 1 && a.row_map == nullptr) {
