@@ -51,7 +51,19 @@ bool pinned_host(const DenseMat& m) {
 // each block of row groups is swept as soon as the x rows up to its largest column
 // index are resident (column watermark), and its y rows leave on the other copy
 // engine -- H2D, sweep and D2H overlap instead of running back to back.
+// Row blocks of the streamed sweep: the transfer of the first x slab(s) and of
+// the last y block are not overlapped, so finer blocks shorten fill and drain
+// (per block: one sweep launch + 2-3 copies, ~10 us).  SELLKIT_STREAM_BLOCKS overrides.
+static int stream_blocks() {
+    static const int nb = [] {
+        const char* e = std::getenv("SELLKIT_STREAM_BLOCKS");
+        return e ? std::max(2, std::atoi(e)) : 64;
+    }();
+    return nb;
+}
+
 static bool spmv_host_streamed(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& o) {
+    const int kStreamBlocks = stream_blocks();
     const bool chain = (o.flags & kFlagChain) != 0;
     const bool ok = pinned_host(x) && pinned_host(y) && (!chain || pinned_host(*o.z));
     if (std::getenv("SELLKIT_VERBOSE"))
@@ -60,7 +72,7 @@ static bool spmv_host_streamed(DenseMat& y, const SellMat& A, const DenseMat& x,
     auto& rt = runtime(A.device);
     rt.copy_streams();
     const gidx ngroups = (gidx(A.nrows_padded) + 31) / 32;
-    const int nb = int(std::min<gidx>(16, ngroups));
+    const int nb = int(std::min<gidx>(kStreamBlocks, ngroups));
     if (nb < 2) return false;
     const std::size_t es = value_bytes(A.dt);
     const lidx w = x.ncols;
