@@ -808,16 +808,23 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
 #pragma unroll
             for (int q = 0; q < 3 * VEC; ++q) dacc[q * NCL + cl] = O::zero();
         }
+        // 32-bit tile/row arithmetic (rows < 2^31: lidx); 64-bit only in the final
+        // address IMAD.WIDEs
+        const int rg0 = int(a.rg0);
+        const int nt = int(ntiles);
+        const int grp_end = int(min(gidx(a.nrows_padded), a.rg1 * 32));  // warps at/after: idle
+        const int row_end = int(min(gidx(a.nrows), a.rg1 * 32));          // rows stored
+        const bool warp_in_tile = warp * WR < rows_per_tile;
         for (int it = 0;; ++it) {
-            const gidx t = seg == 1 ? gidx(it) * gridDim.x + blockIdx.x : tile_of(it, seg);
-            if (t >= ntiles) break;
+            const int t = seg == 1 ? it * int(gridDim.x) + int(blockIdx.x) : int(tile_of(it, seg));
+            if (t >= nt) break;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
-            const gidx row = (a.rg0 + t * rgt) * 32 + rr;
+            const int tile_row0 = (rg0 + t * rgt) * 32;
+            const int row = tile_row0 + rr;
             mbar_wait(&full[s], k & 1u);
             const StageHdr& h = hdr[s];
-            const bool warp_active = warp * WR < rows_per_tile && (a.rg0 + t * rgt) * 32 + warp * WR < a.nrows_padded &&
-                                     (a.rg0 + t * rgt) * 32 + warp * WR < a.rg1 * 32;
+            const bool warp_active = warp_in_tile && tile_row0 + warp * WR < grp_end;
             if (!warp_active) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
@@ -924,16 +931,16 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             if (lane == 0) mbar_arrive(&empty[s]);
             if constexpr (PLAIN) {
                 // y = A x with alpha == 1 and no other flag: t * 1 == t, so the store is the result
-                if (row < a.nrows && row < a.rg1 * 32) {
+                if (row < row_end) {
                     Vec<T, VEC> out;
 #pragma unroll
                     for (int e = 0; e < VEC; ++e) out.v[e] = acc[e];
-                    st_vec<T, VEC>(a.y + row * a.y_rs + sub * VEC, out);
+                    st_vec<T, VEC>(a.y + (unsigned long long)unsigned(row) * unsigned(a.y_rs) + sub * VEC, out);
                 }
                 continue;
             }
             // fused epilogue (spmv_epilogue.hpp:12-36)
-            if (row < a.nrows && row < a.rg1 * 32) {
+            if (row < row_end) {
                 const bool fin = !deferred(a.defer_mask, row);
                 const int cb = sub * VEC;
                 T* yp = a.y + row * a.y_rs + cb;
