@@ -655,34 +655,41 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
     }
 }
 
-// Occupancy of the row-contiguous kernel.  The consumers are latency bound (each
-// warp has one batch of gathers in flight, then computes), so resident warps are
-// worth more than unroll depth or stage depth: measured on B200 (400^3, w = 8),
-// 2 CTAs/SM x 3 stages x U = 8: 3.46 ms; 3 CTAs x 3 x U = 4: 2.55 ms;
-// 4 CTAs x 2 stages x U = 3: 2.47 ms.  The dots variant keeps 3 x VEC extra
-// accumulators live and runs at one CTA less.
+// Occupancy and staging of the row-contiguous kernel.  The consumers are latency
+// bound (each warp has one batch of gathers in flight, then computes), so resident
+// warps are worth more than unroll depth: measured on B200 (400^3, w = 8),
+// 2 CTAs/SM x U = 8: 3.46 ms; 3 CTAs x U = 4: 2.55 ms; 4 CTAs x U = 3: 2.47 ms.
+// Stages hold one full tile (kNCW * WR rows) of a 7-nonzero stencil and no more,
+// so shared memory does not take L1 from the RHS gathers: 3 x 11 KB for
+// multi-lane rows (w = 8: 2 x 16 KB 2.55 ms -> 3 x 11 KB 2.31 ms), 2 x 22 KB when a
+// lane owns a whole RHS row (TPR = 1, 256-row tiles).  Longer rows shrink the
+// tile (fewer active warps) or, past a stage, read the matrix from global memory.
+// The sizes are compile-time: the same kernel with runtime stage sizes was
+// scheduled worse by ptxas (2.8 ms, products hoisted between the gathers).
 #ifndef SK_RMINB
 #define SK_RMINB 4
 #endif
 #ifndef SK_RMINB_DOTS
 #define SK_RMINB_DOTS 3
 #endif
-#ifndef SK_RSTAGES
-#define SK_RSTAGES 2
+#ifndef SK_RSTAGES_WIDE
+#define SK_RSTAGES_WIDE 3
+#endif
+#ifndef SK_RSTAGES_NARROW
+#define SK_RSTAGES_NARROW 2
 #endif
 #ifndef SK_RSTAGE_KB
-#define SK_RSTAGE_KB 16
+#define SK_RSTAGE_KB 11
 #endif
 #ifndef SK_RSTAGE_KB_NARROW
-#define SK_RSTAGE_KB_NARROW 24
+#define SK_RSTAGE_KB_NARROW 22
 #endif
-constexpr int kRStages = SK_RSTAGES;
 
-// Stage size: a tile is kNCW * WR rows, so narrow blocks (WR = 32) need deeper
-// stages to give every consumer warp its rows.
 template <class T, int W>
 struct RGeom {
-    static constexpr int SB = (W * int(sizeof(T)) >= 32 ? SK_RSTAGE_KB : SK_RSTAGE_KB_NARROW) * 1024;
+    static constexpr bool WIDE = RPlan<T, W>::TPR > 1;
+    static constexpr int STAGES = WIDE ? SK_RSTAGES_WIDE : SK_RSTAGES_NARROW;
+    static constexpr int SB = (WIDE ? SK_RSTAGE_KB : SK_RSTAGE_KB_NARROW) * 1024;
     static constexpr int SCAP = (SB / int(sizeof(T) + 4)) / 32 * 32;  // slots per stage
 };
 
@@ -690,8 +697,8 @@ struct RGeom {
 // dacc[3][VEC][consumer lanes] (lane-contiguous: conflict-free)
 template <class T, int W>
 constexpr std::size_t rows_stage_bytes() {
-    return (std::size_t(kRStages) * RGeom<T, W>::SB + std::size_t(kRStages) * sizeof(StageHdr) + 2 * kRStages * 8 + 15) /
-           16 * 16;
+    constexpr int S = RGeom<T, W>::STAGES;
+    return (std::size_t(S) * RGeom<T, W>::SB + std::size_t(S) * sizeof(StageHdr) + 2 * S * 8 + 15) / 16 * 16;
 }
 template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
@@ -706,7 +713,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
     constexpr int VEC = P::VEC, TPR = P::TPR, WR = P::WR;
     constexpr int SCAP = RGeom<T, W>::SCAP;
     constexpr int SB = RGeom<T, W>::SB;
-    constexpr int kStages = kRStages;
+    constexpr int kStages = RGeom<T, W>::STAGES;
     static_assert(32 % C == 0, "chunk height must divide the warp");
     auto tile_of = [&](int it, int sg) -> gidx {
         const gidx q = it / sg, w = it % sg;
