@@ -52,3 +52,30 @@ def test_stencil_fullsize_exact(sk, n, w):
     torch.cuda.synchronize()
     want = 0.5 * (Yref - 0.25 * Xs) - y0
     assert torch.equal(Ys, want)
+
+
+@pytest.mark.parametrize("n,m,k", [(100_000_000, 8, 8), (20_000_000, 64, 64), (50_000_000, 16, 32)])
+def test_tsm_fullsize_exact(sk, n, m, k):
+    """C4 sizes: small-integer V, W, X make TSMM / TSMTTSM exact in FP64 (every partial
+    sum is an integer below 2^53), so any summation order must match torch bit for bit."""
+    import torch
+    from paper_1507_08101_b200 import sellkit
+    dev = torch.device("cuda")
+    r = torch.arange(n, device=dev, dtype=torch.int64)[:, None]
+    V = ((r * 3 + torch.arange(m, device=dev)[None, :] * 5) % 7 - 3).to(torch.float64)
+    W = ((r * 5 + torch.arange(k, device=dev)[None, :] * 3) % 9 - 4).to(torch.float64)
+    X = ((torch.arange(m * k, device=dev) * 7) % 11 - 5).to(torch.float64).view(m, k).contiguous()
+    v = sk.view_plain(V.data_ptr(), n * m, n, m, m, keep=V)
+    wv = sk.view_plain(W.data_ptr(), n * k, n, k, k, keep=W)
+    Xo = torch.zeros(m, k, dtype=torch.float64, device=dev)
+    x = sk.view_plain(Xo.data_ptr(), m * k, m, k, k, keep=Xo)
+    one, zero = np.array([1.0]), np.array([0.0])
+    sk.call("sellkit_tsmttsm", x.h, v.h, wv.h, one.ctypes.data, zero.ctypes.data, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(Xo, V.T @ W)
+    Xs = sk.view_plain(X.data_ptr(), m * k, m, k, k, keep=X)
+    Wout = torch.empty(n, k, dtype=torch.float64, device=dev)
+    wo = sk.view_plain(Wout.data_ptr(), n * k, n, k, k, keep=Wout)
+    sk.call("sellkit_tsmm", wo.h, v.h, Xs.h, one.ctypes.data, zero.ctypes.data)
+    torch.cuda.synchronize()
+    assert torch.equal(Wout, V @ X)
