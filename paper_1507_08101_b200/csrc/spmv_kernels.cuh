@@ -685,6 +685,10 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 #define SK_RSTAGE_KB_NARROW 22
 #endif
 
+#ifndef SK_RTILE_ROWS
+#define SK_RTILE_ROWS 128
+#endif
+
 template <class T, int W>
 struct RGeom {
     static constexpr bool WIDE = RPlan<T, W>::TPR > 1;
@@ -799,7 +803,6 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
         // ------------------------------------------------------- consumer warps
         const int sub = lane % TPR;
         const int rl = lane / TPR;
-        const int rr = warp * WR + rl;  // row within the tile
         const bool need_x = (a.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
         const unsigned xrs = unsigned(a.x_rs);
         const T* xb = a.x + sub * VEC;
@@ -821,22 +824,25 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
         const int nt = int(ntiles);
         const int grp_end = int(min(gidx(a.nrows_padded), a.rg1 * 32));  // warps at/after: idle
         const int row_end = int(min(gidx(a.nrows), a.rg1 * 32));          // rows stored
-        const bool warp_in_tile = warp * WR < rows_per_tile;
+        // (compile-time bound: one pass for the dots variant, whose register budget
+        // has no room for the pass loop -- measured 30 % slower on C3 C64)
+        constexpr int kMaxPasses = DOTS ? 1 : (SK_RTILE_ROWS / (kNCW * WR) > 1 ? SK_RTILE_ROWS / (kNCW * WR) : 1);
+        const int passes = min(kMaxPasses, (rows_per_tile + kNCW * WR - 1) / (kNCW * WR));
         for (int it = 0;; ++it) {
             const int t = seg == 1 ? it * int(gridDim.x) + int(blockIdx.x) : int(tile_of(it, seg));
             if (t >= nt) break;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
             const int tile_row0 = (rg0 + t * rgt) * 32;
-            const int row = tile_row0 + rr;
             mbar_wait(&full[s], k & 1u);
             const StageHdr& h = hdr[s];
-            const bool warp_active = warp_in_tile && tile_row0 + warp * WR < grp_end;
-            if (!warp_active) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                continue;
-            }
+            // a tile may hold several warp-row passes (narrow warps, short rows): the
+            // per-tile work (barrier, header, release) is shared by all of them
+            for (int pass = 0; pass < passes; ++pass) {
+            const int wrow0 = (pass * kNCW + warp) * WR;  // this warp's first row of the pass
+            if (wrow0 >= rows_per_tile || tile_row0 + wrow0 >= grp_end) break;  // warp-uniform
+            const int rr = wrow0 + rl;
+            const int row = tile_row0 + rr;
             const int cq = rr / C;
             const int ip = rr % C;
             const lidx len = cq < h.nchunks ? h.hlen[cq] : 0;
@@ -934,8 +940,6 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 gather(reinterpret_cast<const T*>(smem + s * SB), reinterpret_cast<const lidx*>(smem + s * SB + SCAP * sizeof(T)));
             else
                 gather(a.val + h.off0, a.col + h.off0);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
             if constexpr (PLAIN) {
                 // y = A x with alpha == 1 and no other flag: t * 1 == t, so the store is the result
                 if (row < row_end) {
@@ -991,6 +995,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                     }
                 }
             }
+            }  // pass
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // matrix data of the tile consumed
         }
         if constexpr (DOTS) {
             // lanes of a row slot -> warp total per column (fixed butterfly order)
@@ -1233,10 +1240,14 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
         const bool rows = rm != 0;
         const bool stride_ok = gidx(a.x_rs) * gidx(sizeof(T)) < (gidx(1) << 31);  // 32-bit byte stride
         if (rows && stride_ok && kernel_mode() != 1 && a.row_map == nullptr) {
+            // tiles of at least SK_RTILE_ROWS rows (several warp passes when a warp's
+            // rows are few), as far as one stage holds them
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
-            const int rgt = std::min(kNCW * RPlan<T, W>::WR / 32, cap);
+            const bool dots = (a.flags & kFlagDots) != 0;
+            const int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
+                                     cap);
             if (rgt >= 1) {
-                if (a.flags & kFlagDots) return launch_tma_rows<T, C, W, true, false>(a, rgt, rt, st);
+                if (dots) return launch_tma_rows<T, C, W, true, false>(a, rgt, rt, st);
                 // plain y = A x: no flag, alpha == 1, no deferred rows
                 const T one = Ops<T>::one();
                 static const bool no_plain = std::getenv("SELLKIT_SPMV_NOPLAIN") != nullptr;  // A/B switch
