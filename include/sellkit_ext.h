@@ -61,6 +61,16 @@ sellkit_error sellkit_ext_mat_export(const sellkit_mat* m, int32_t* row_perm_inv
                                      int32_t* rowlen, int32_t* chunk_len, int64_t* chunk_offset,
                                      void* val, int32_t* col);
 
+/* Sweep order for SpMV/SpMMV over the whole matrix (results are independent of it;
+ * dot products may differ in the last bits): the stored rows are split into blocks
+ * of block_rows (a multiple of 32) and swept in the order order[0..nblocks) (a
+ * permutation of the block indices, nblocks = ceil(nrows_padded / block_rows)).
+ * Used to keep the RHS reuse window small for matrices whose coupling distance is
+ * long in row order (e.g. a pencil order over a 3-D lattice).  order == NULL
+ * restores the natural order. */
+sellkit_error sellkit_ext_mat_set_sweep_order(sellkit_mat* m, sellkit_lidx block_rows, const int32_t* order,
+                                              sellkit_gidx nblocks);
+
 /* ------------------------------------------------------- dense matrices -- */
 sellkit_error sellkit_ext_densemat_storage(const sellkit_densemat* m, void** data, sellkit_lidx* stride,
                                            int* order, int* device, int* on_device);

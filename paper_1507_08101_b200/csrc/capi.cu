@@ -698,6 +698,38 @@ sellkit_error sellkit_ext_mat_export(const sellkit_mat* m, int32_t* row_perm_inv
     });
 }
 
+sellkit_error sellkit_ext_mat_set_sweep_order(sellkit_mat* m, sellkit_lidx block_rows, const int32_t* order,
+                                              sellkit_gidx nblocks) {
+    return guarded([&] {
+        require(m != nullptr, "null handle");
+        auto& a = *m->p;
+        if (!order) {
+            a.sweep_order = sk::DeviceBuffer();
+            a.sweep_block_rgs = 0;
+            a.sweep_blocks = 0;
+            return;
+        }
+        SK_REQUIRE(block_rows > 0 && block_rows % 32 == 0 && block_rows <= 32 * 4096, sk::errc::invalid_arg,
+                   "block_rows must be a positive multiple of 32");
+        const sellkit_gidx want = (sellkit_gidx(a.nrows_padded) + block_rows - 1) / block_rows;
+        SK_REQUIRE(nblocks == want, sk::errc::shape_mismatch, "nblocks must be ceil(nrows_padded / block_rows)");
+        std::vector<char> seen(std::size_t(nblocks), 0);
+        for (sellkit_gidx i = 0; i < nblocks; ++i) {
+            SK_REQUIRE(order[i] >= 0 && order[i] < nblocks && !seen[std::size_t(order[i])], sk::errc::invalid_arg,
+                       "order must be a permutation of the block indices");
+            seen[std::size_t(order[i])] = 1;
+        }
+        sk::DeviceGuard g(a.device);
+        auto& rt = sk::runtime(a.device);
+        sk::DeviceBuffer buf(std::size_t(nblocks) * sizeof(int32_t), a.device);
+        CK(cudaMemcpyAsync(buf.get(), order, std::size_t(nblocks) * sizeof(int32_t), cudaMemcpyHostToDevice, rt.stream));
+        CK(cudaStreamSynchronize(rt.stream));
+        a.sweep_order = std::move(buf);
+        a.sweep_block_rgs = int(block_rows / 32);
+        a.sweep_blocks = nblocks;
+    });
+}
+
 sellkit_error sellkit_ext_densemat_storage(const sellkit_densemat* m, void** data, sellkit_lidx* stride, int* order,
                                            int* device, int* on_device) {
     return guarded([&] {

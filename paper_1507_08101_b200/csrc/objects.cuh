@@ -49,6 +49,11 @@ struct SellMat {
     DeviceBuffer row_perm;      // int32 [nrows]   original -> stored
     DeviceBuffer row_perm_inv;  // int32 [nrows]   stored -> original
     DeviceBuffer rowlen;        // int32 [nrows_padded]
+    // optional sweep order of the row-contiguous kernel: blocks of sweep_block_rgs row
+    // groups (32 stored rows each) visited in sweep_order[] (sellkit_ext_mat_set_sweep_order)
+    DeviceBuffer sweep_order;   // int32 [sweep_blocks]
+    int sweep_block_rgs = 0;
+    gidx sweep_blocks = 0;
     // streamed host-buffer spmv: largest column index per row-group block (lazily computed)
     mutable std::vector<lidx> watermark;
     mutable int watermark_blocks = 0;

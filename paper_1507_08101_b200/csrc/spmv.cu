@@ -271,6 +271,10 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         a.row_map = hooks.row_map;
         a.rg0 = hooks.rg0;
         a.rg1 = hooks.rg1 < 0 ? (gidx(A.nrows_padded) + 31) / 32 : hooks.rg1;
+        if (A.sweep_block_rgs > 0 && hooks.rg0 == 0 && hooks.rg1 < 0 && hooks.row_map == nullptr) {
+            a.sweep_order = A.sweep_order.as<int>();  // full sweep: the matrix's block order
+            a.sweep_brg = A.sweep_block_rgs;
+        }
 
         // scratch: [gamma_list W][final dots 3W][partials]
         const std::size_t max_parts = std::size_t(rt.num_sms) * 32 * std::size_t((W + kGW - 1) / kGW + 1);

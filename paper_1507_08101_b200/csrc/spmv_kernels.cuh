@@ -68,6 +68,8 @@ struct KArgs {
     const std::uint32_t* defer_mask;
     const lidx* row_map;
     gidx rg0, rg1;  // row groups (32 stored rows each) [rg0, rg1) swept by this launch
+    const int* sweep_order;  // full sweeps only: blocks of sweep_brg row groups in this order
+    int sweep_brg;           // 0 = natural order
 };
 
 namespace spmv_detail {
@@ -313,6 +315,7 @@ struct StageHdr {
     int overflow;                  // tile did not fit the stage: read from global
     int nchunks;
     long long off0;                // absolute slot offset of the tile
+    int row0;                      // first stored row of the tile (rows kernel)
 };
 
 // Work split of the TMA kernel: every consumer warp owns one 32-B column slice of
@@ -741,6 +744,12 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
     const int chunks_per_tile = rgt * (32 / C);
     const int rows_per_tile = rgt * 32;
     constexpr bool want_dots = DOTS;  // launch selects DOTS == (flags & kFlagDots) != 0
+    // first row group of tile t: natural order, or the caller's block order (locality)
+    const int tpb = a.sweep_brg > 0 ? a.sweep_brg / rgt : 1;
+    auto tile_rg = [&](gidx t) -> gidx {
+        if (a.sweep_brg > 0) return gidx(__ldg(a.sweep_order + t / tpb)) * a.sweep_brg + (t % tpb) * rgt;
+        return a.rg0 + t * rgt;
+    };
 
     if (warp == kNCW) {
         // ------------------------------------------------- producer warp (as spmv_tma_kernel)
@@ -754,7 +763,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             // prefetch each, a stage ahead of the consumers, so the epilogue reads
             // hit L2 instead of adding a dependent HBM round trip per tile
             if (kPrefetchEpi && lane == 0 && (a.flags & (kFlagAxpby | kFlagChain))) {
-                const gidx r0 = (a.rg0 + t * rgt) * 32;
+                const gidx r0 = tile_rg(t) * 32;
                 const gidx r1 = min(r0 + gidx(rows_per_tile), min(gidx(a.nrows), a.rg1 * 32));
                 auto span = [&](const T* base, gidx rs) {
                     const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(base + r0 * rs) & ~std::uintptr_t(15);
@@ -771,7 +780,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 }
             }
             mbar_wait(&empty[s], (k & 1u) ^ 1u);
-            const gidx c0 = a.rg0 * (32 / C) + t * chunks_per_tile;
+            const gidx c0 = tile_rg(t) * (32 / C);
             const gidx c1 = min(min(a.nchunks, a.rg1 * (32 / C)), c0 + chunks_per_tile);
             const int nc = int(c1 - c0);
             const gidx off0 = a.chunk_offset[c0];
@@ -783,6 +792,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 hdr[s].overflow = fits ? 0 : 1;
                 hdr[s].nchunks = nc;
                 hdr[s].off0 = off0;
+                hdr[s].row0 = int(c0 / (32 / C)) * 32;
             }
             __syncwarp();
             if (lane == 0) {
@@ -833,9 +843,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             if (t >= nt) break;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
-            const int tile_row0 = (rg0 + t * rgt) * 32;
             mbar_wait(&full[s], k & 1u);
             const StageHdr& h = hdr[s];
+            const int tile_row0 = h.row0;  // the producer resolved the sweep order
             // a tile may hold several warp-row passes (narrow warps, short rows): the
             // per-tile work (barrier, header, release) is shared by all of them
             for (int pass = 0; pass < passes; ++pass) {
@@ -1221,7 +1231,9 @@ LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaS
         return std::max(nb, 1);
     }();
     const gidx ngroups = a.rg1 - a.rg0;
-    const gidx ntiles = (ngroups + rgt - 1) / rgt;
+    // with a sweep order, tiles never straddle a block: blocks x (block / tile) tiles
+    const gidx blocks = a.sweep_brg > 0 ? (ngroups + a.sweep_brg - 1) / a.sweep_brg : 0;
+    const gidx ntiles = a.sweep_brg > 0 ? blocks * (a.sweep_brg / rgt) : (ngroups + rgt - 1) / rgt;
     const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
     static const int seg = [] {
         const char* e = std::getenv("SELLKIT_TMA_SEG");
@@ -1244,8 +1256,9 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
             // rows are few), as far as one stage holds them
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
             const bool dots = (a.flags & kFlagDots) != 0;
-            const int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
-                                     cap);
+            int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
+                               cap);
+            while (a.sweep_brg > 0 && rgt > 1 && a.sweep_brg % rgt != 0) --rgt;  // tiles inside blocks
             if (rgt >= 1) {
                 if (dots) return launch_tma_rows<T, C, W, true, false>(a, rgt, rt, st);
                 // plain y = A x: no flag, alpha == 1, no deferred rows

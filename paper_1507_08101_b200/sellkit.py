@@ -152,6 +152,7 @@ _EXT = [
     ("sellkit_ext_mat_info", err_t, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(lidx), C.POINTER(gidx),
                                      C.POINTER(gidx), C.POINTER(C.c_int)]),
     ("sellkit_ext_mat_export", err_t, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    ("sellkit_ext_mat_set_sweep_order", err_t, [vp, lidx, vp, gidx]),
     ("sellkit_ext_densemat_storage", err_t, [vp, C.POINTER(vp), C.POINTER(lidx), C.POINTER(C.c_int),
                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("sellkit_ext_densemat_fill_hash", err_t, [vp, C.c_uint64]),
@@ -374,6 +375,14 @@ class Mat(_Handle):
                      C.byref(sl), C.byref(cp))
         return dict(C=ch.value, sigma=sg.value, nrows_padded=nrp.value, nchunks=nch.value, slots=sl.value,
                     cols_permuted=cp.value)
+
+    def set_sweep_order(self, block_rows: int, order: Optional[np.ndarray]):
+        """Sweep blocks of `block_rows` stored rows in `order` (None: natural order)."""
+        if order is None:
+            self.sk.call("sellkit_ext_mat_set_sweep_order", self.h, block_rows, None, 0)
+            return
+        o = np.ascontiguousarray(order, np.int32)
+        self.sk.call("sellkit_ext_mat_set_sweep_order", self.h, block_rows, _ptr(o), len(o))
 
     def export(self) -> dict:
         """SELL arrays (sellkit_ext_mat_export)."""

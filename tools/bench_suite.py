@@ -18,6 +18,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1507_08101_b200 import sellkit  # noqa: E402
+from paper_1507_08101_b200.orders import pencil_order  # noqa: E402
 
 sk = sellkit.load()
 stream = torch.cuda.ExternalStream(sk.stream())
@@ -101,11 +102,15 @@ def c3():
 
         def fn():
             sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, dot=dots)
-        ms = timed(fn, reps=5)
         alg = (vb + 4.0) * nnz + vb * w * N * 3  # x read, y read + write
         fl = (8.0 if dt == sellkit.C64 else 2.0) * nnz * w
-        emit(case=f"c3 TI KPM step 2^24 rows w=16 {'C64' if dt == sellkit.C64 else 'R64'}", ms=ms,
-             gflops=fl / ms / 1e6, gbs=alg / ms / 1e6, frac=alg / ms / 1e6 / PEAK)
+        # natural row order, then a pencil sweep order (orders.py: z-reuse window of yb x-lines)
+        for order in ("rows", "pencil16"):
+            if order != "rows":
+                A.set_sweep_order(256, pencil_order(lx, ly, lz, per_site=4, block_rows=256, yb=16))
+            ms = timed(fn, reps=5)
+            emit(case=f"c3 TI KPM step 2^24 rows w=16 {'C64' if dt == sellkit.C64 else 'R64'}", order=order, ms=ms,
+                 gflops=fl / ms / 1e6, gbs=alg / ms / 1e6, frac=alg / ms / 1e6 / PEAK)
         del A, x, y
 
 
