@@ -641,6 +641,14 @@ struct RPlan {
     static constexpr bool ok = TPR >= 1 && TPR <= 8 && W % VEC == 0 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0;
 };
 
+// Per-lane shared-memory dot slot += v.  Only the owning lane touches a slot, so the
+// order of additions is fixed.  (A shared-memory atomicAdd on doubles compiles to a
+// compare-and-swap loop on sm_100a, so the plain read-add-write is kept.)
+template <class T>
+__device__ __forceinline__ void slot_add(T* p, T v) {
+    *p = Ops<T>::add(*p, v);
+}
+
 // Remainder handling of the row-contiguous kernel: 0 = exact-size batch when the
 // row length is warp-uniform, 1 = predicated batch, 2 = predicated loads too.
 #ifndef SK_TAILMODE
@@ -996,11 +1004,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) {
                             T* dp = dacc + e * NCL + cl;
-                            if (a.flags & kFlagDotYY) dp[0] = O::add(dp[0], O::mul(O::conj(out.v[e]), out.v[e]));
-                            if (a.flags & kFlagDotXY)
-                                dp[VEC * NCL] = O::add(dp[VEC * NCL], O::mul(O::conj(xs.v[e]), out.v[e]));
-                            if (a.flags & kFlagDotXX)
-                                dp[2 * VEC * NCL] = O::add(dp[2 * VEC * NCL], O::mul(O::conj(xs.v[e]), xs.v[e]));
+                            if (a.flags & kFlagDotYY) slot_add(dp, O::mul(O::conj(out.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXY) slot_add(dp + VEC * NCL, O::mul(O::conj(xs.v[e]), out.v[e]));
+                            if (a.flags & kFlagDotXX) slot_add(dp + 2 * VEC * NCL, O::mul(O::conj(xs.v[e]), xs.v[e]));
                         }
                     }
                 }
