@@ -651,6 +651,9 @@ __device__ __forceinline__ void slot_add(T* p, T v) {
 
 // Remainder handling of the row-contiguous kernel: 0 = exact-size batch when the
 // row length is warp-uniform, 1 = predicated batch, 2 = predicated loads too.
+#ifndef SK_BATCH_UNROLL1
+#define SK_BATCH_UNROLL1 0
+#endif
 #ifndef SK_TAILMODE
 #define SK_TAILMODE 0
 #endif
@@ -909,6 +912,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                     cp += R * C;
                 };
                 lidx j0 = 0;
+#if SK_BATCH_UNROLL1
+#pragma unroll 1
+#endif
                 for (; j0 + U <= minlen; j0 += U) batch(std::integral_constant<int, U>{});
                 if (SK_TAILMODE == 0 && minlen == maxlen) {
                     // warp-uniform row length (every row of the warp in one chunk, the usual

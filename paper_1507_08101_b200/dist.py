@@ -334,3 +334,52 @@ def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank
     return BenchJob(step=step, e2e_step=e2e_step, rows_local=nloc, nnz_local=nnz_local, halo_bytes=halo_bytes,
                     launches_per_step=launches, h2d_bytes=nloc * w * 8, d2h_bytes=nloc * w * 8,
                     keep=[rc, x, y, xh, yh, opts])
+
+
+# ------------------------------------------------------- tall-skinny, sharded
+# SURVEY §8(e): TSMM is row-sharded with no communication (X replicated); TSMTTSM
+# is row-sharded with one exchange of the m x k partials.  The reference has no
+# distributed TSMTTSM; here every rank gathers all partials and sums them in rank
+# order with the library's axpby, so every rank holds the identical (deterministic)
+# result, as the reference's rank-ordered allreduce of dots does (partition.hpp:379-394).
+
+def gather_in_rank_order(t, group=None) -> list:
+    """[t_0, ..., t_{k-1}] from every rank (all_gather; works for gloo CPU and NCCL GPU tensors)."""
+    import torch
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size(group) == 1:
+        return [t]
+    parts = [torch.empty_like(t) for _ in range(tdist.get_world_size(group))]
+    tdist.all_gather(parts, t.contiguous(), group=group)
+    return parts
+
+
+def tsmm(sk: Sellkit, w, v, x, alpha=1.0, beta=0.0):
+    """W_r = alpha V_r X + beta W_r on this rank's rows (X replicated): no communication."""
+    dt = w.dt
+    a = np.atleast_1d(np.asarray(alpha, sellkit.NP_DTYPE[dt]))
+    b = np.atleast_1d(np.asarray(beta, sellkit.NP_DTYPE[dt]))
+    sk.call("sellkit_tsmm", w, v, x, _ptr(a), _ptr(b))
+
+
+def tsmttsm(sk: Sellkit, x, v, w, alpha=1.0, beta=0.0, kahan: bool = False, group=None):
+    """X = alpha * sum_r V_r^H W_r + beta X over row-sharded V, W (one shard per rank)."""
+    import torch
+    dt = x.dt
+    npdt = sellkit.NP_DTYPE[dt]
+    tdt = {sellkit.R32: torch.float32, sellkit.R64: torch.float64, sellkit.C32: torch.complex64,
+           sellkit.C64: torch.complex128}[dt]
+    m, k = x.dims()
+    one, zero = np.ones(1, npdt), np.zeros(1, npdt)
+    part = torch.zeros((m, k), dtype=tdt, device="cuda")
+    pv = sk.view_plain(part.data_ptr(), m * k, m, k, k, dt=dt, keep=part)
+    sk.call("sellkit_tsmttsm", pv, v, w, _ptr(one), _ptr(zero), 1 if kahan else 0)  # V_r^H W_r
+    parts = gather_in_rank_order(part, group)
+    acc = parts[0].clone()
+    av = sk.view_plain(acc.data_ptr(), m * k, m, k, k, dt=dt, keep=acc)
+    for p in parts[1:]:
+        sk.call("sellkit_axpby", av, sk.view_plain(p.data_ptr(), m * k, m, k, k, dt=dt, keep=p), _ptr(one),
+                _ptr(one))
+    a = np.atleast_1d(np.asarray(alpha, npdt))
+    b = np.atleast_1d(np.asarray(beta, npdt))
+    sk.call("sellkit_axpby", x, av, _ptr(a), _ptr(b))  # X = alpha * sum + beta * X

@@ -120,3 +120,35 @@ def test_multiprocess_request_exchange_gloo():
         p.join(timeout=60)
     for rank, ok, msg in res:
         assert ok, (rank, msg)
+
+
+def _gather_worker(rank, world, port, q):
+    try:
+        import torch
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        from paper_1507_08101_b200.dist import gather_in_rank_order
+        t = torch.full((3, 2), float(rank + 1), dtype=torch.float64)
+        parts = gather_in_rank_order(t)
+        ok = len(parts) == world and all(bool(torch.all(p == r + 1)) for r, p in enumerate(parts))
+        tdist.destroy_process_group()
+        q.put((rank, ok, ""))
+    except Exception as exc:  # pragma: no cover
+        q.put((rank, False, repr(exc)))
+
+
+def test_tsmttsm_partials_gathered_in_rank_order_gloo():
+    """Sharded TSMTTSM plumbing: every rank receives all m x k partials
+    in rank order (gloo, world size 3), so the ordered sum is identical on every rank."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, msg in res:
+        assert ok, (rank, msg)

@@ -161,3 +161,20 @@ def test_blas1(sk, orc):
     assert cc.tolist() == cv.tolist()
     for h in (vh, ch, conv):
         sk.lib.sellkit_densemat_destroy(h)
+
+
+def test_sharded_tsm_wrappers_single_rank(sk, orc):
+    """dist.tsmttsm / dist.tsmm at world size 1 equal the local kernels."""
+    from paper_1507_08101_b200 import dist
+    rng = np.random.default_rng(9)
+    n, m, k = 5000, 16, 8
+    V, W, X = rng.uniform(-1, 1, (n, m)), rng.uniform(-1, 1, (n, k)), rng.uniform(-1, 1, (m, k))
+    x, v, w = sk.densemat_from(X), sk.densemat_from(V), sk.densemat_from(W)
+    dist.tsmttsm(sk, x, v, w, alpha=0.75, beta=0.5)
+    want = orc.tsmttsm(V, W, X, 0.75, 0.5)
+    scale = np.abs(V).T @ np.abs(W)
+    assert np.all(np.abs(x.copy_out() - want) <= 1e-12 * (1 + scale + np.abs(X)))
+    w2 = sk.densemat_from(W)
+    xs = sk.densemat_from(X[:m, :k])
+    dist.tsmm(sk, w2, v, xs, alpha=1.5, beta=-0.5)
+    assert np.max(np.abs(w2.copy_out() - (1.5 * V @ X - 0.5 * W)) / (1 + np.abs(W))) < 1e-12
