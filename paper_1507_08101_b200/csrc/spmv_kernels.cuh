@@ -703,24 +703,30 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 #define SK_RTILE_ROWS 128
 #endif
 
-template <class T, int W>
+#ifndef SK_RSTAGES_DOTS
+#define SK_RSTAGES_DOTS 0  // 0: as the plain kernel
+#endif
+
+template <class T, int W, bool DOTS = false>
 struct RGeom {
     static constexpr bool WIDE = RPlan<T, W>::TPR > 1;
-    static constexpr int STAGES = WIDE ? SK_RSTAGES_WIDE : SK_RSTAGES_NARROW;
+    static constexpr int STAGES =
+        (DOTS && SK_RSTAGES_DOTS > 0) ? SK_RSTAGES_DOTS : (WIDE ? SK_RSTAGES_WIDE : SK_RSTAGES_NARROW);
     static constexpr int SB = (WIDE ? SK_RSTAGE_KB : SK_RSTAGE_KB_NARROW) * 1024;
     static constexpr int SCAP = (SB / int(sizeof(T) + 4)) / 32 * 32;  // slots per stage
 };
 
 // stage ring, headers, barriers; with dots also the per-lane dot accumulators
 // dacc[3][VEC][consumer lanes] (lane-contiguous: conflict-free)
-template <class T, int W>
+template <class T, int W, bool DOTS>
 constexpr std::size_t rows_stage_bytes() {
-    constexpr int S = RGeom<T, W>::STAGES;
+    constexpr int S = RGeom<T, W, DOTS>::STAGES;
     return (std::size_t(S) * RGeom<T, W>::SB + std::size_t(S) * sizeof(StageHdr) + 2 * S * 8 + 15) / 16 * 16;
 }
 template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
-    return rows_stage_bytes<T, W>() + (DOTS ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) + 128;
+    return rows_stage_bytes<T, W, DOTS>() + (DOTS ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) +
+           128;
 }
 
 template <class T, int C, int W, int U, bool DOTS, bool PLAIN>
@@ -731,7 +737,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
     constexpr int VEC = P::VEC, TPR = P::TPR, WR = P::WR;
     constexpr int SCAP = RGeom<T, W>::SCAP;
     constexpr int SB = RGeom<T, W>::SB;
-    constexpr int kStages = RGeom<T, W>::STAGES;
+    constexpr int kStages = RGeom<T, W, DOTS>::STAGES;
     static_assert(32 % C == 0, "chunk height must divide the warp");
     auto tile_of = [&](int it, int sg) -> gidx {
         const gidx q = it / sg, w = it % sg;
@@ -832,7 +838,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
         // column dots: every lane accumulates its rows' terms in its own shared-memory
         // slots (no 3 x VEC accumulators live across the gather loop); the lanes are
         // reduced once at the end, in a fixed order (deterministic)
-        T* dacc = reinterpret_cast<T*>(smem + rows_stage_bytes<T, W>());
+        T* dacc = reinterpret_cast<T*>(smem + rows_stage_bytes<T, W, DOTS>());
         const int cl = warp * 32 + lane;  // consumer lane
         constexpr int NCL = kNCW * 32;
         if constexpr (DOTS) {
