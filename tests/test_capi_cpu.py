@@ -139,3 +139,22 @@ def test_num_workers_and_timer(sk):
     assert sk.lib.sellkit_set_num_workers(0) == sellkit.ERR_INVALID_ARG
     t0 = sk.lib.sellkit_now_seconds()
     assert t0 > 0
+
+
+def test_pencil_order_is_a_block_permutation():
+    """orders.pencil_order: a permutation of the row blocks; consecutive z of one y-slab
+    are adjacent in the sweep (the property that shrinks the RHS reuse window)."""
+    import numpy as np
+    from paper_1507_08101_b200.orders import pencil_order
+    lx, ly, lz, per = 64, 8, 6, 4
+    o = pencil_order(lx, ly, lz, per_site=per, block_rows=256, yb=2)
+    nblocks = lx * ly * lz * per // 256
+    assert sorted(o.tolist()) == list(range(nblocks))
+    bpl = lx * per // 256
+    # first slab: y in {0, 1}, all z, before any y >= 2
+    first = o[: lz * 2 * bpl]
+    ys = (first // bpl) % ly
+    assert set(ys.tolist()) == {0, 1}
+    import pytest
+    with pytest.raises(ValueError):
+        pencil_order(10, 4, 4, per_site=1, block_rows=32)
