@@ -339,7 +339,9 @@ void rank_sweeps(RankPart& part, RankScratch& sc, DenseMat& y, const DenseMat& x
     hl.stream = st;
     hl.accumulate_dots = true;
     hl.dot_accum = sc.dots.get();
-    if (has_remote) hl.defer_mask = part.defer_mask.as<std::uint32_t>();
+    // rows finished by the remote sweep contribute their dots/chain there; without dots
+    // or chain the mask is not needed and the local sweep runs the plain y = A x kernel
+    if (has_remote && (dots || chain)) hl.defer_mask = part.defer_mask.as<std::uint32_t>();
     CK(cudaMemsetAsync(sc.dots.get(), 0, 3 * std::size_t(x.ncols) * value_bytes(part.plan.dt), st));
     spmv_device(y, *part.local, x, base, hl);
     if (!has_remote) return;
