@@ -658,6 +658,17 @@ __device__ __forceinline__ void slot_add(T* p, T v) {
 #define SK_TAILMODE 0
 #endif
 
+// acc + v * x: two separately rounded operations (the reference's arithmetic, bit-exact)
+// or, with SK_SPMV_FMA, one fused multiply-add (within the 1e-12 tolerance).
+#ifndef SK_SPMV_FMA
+#define SK_SPMV_FMA 0
+#endif
+template <class T>
+__device__ __forceinline__ T mac(T acc, T v, T x) {
+    if constexpr (SK_SPMV_FMA) return Ops<T>::fma(v, x, acc);
+    else return Ops<T>::add(acc, Ops<T>::mul(v, x));
+}
+
 // f(integral_constant<R>) for the runtime remainder r in [1, RMAX] (r == 0: nothing)
 template <int RMAX, class F>
 __device__ __forceinline__ void tail_dispatch(int r, F& f) {
@@ -913,7 +924,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
 #pragma unroll
                     for (int u = 0; u < R; ++u)
 #pragma unroll
-                        for (int e = 0; e < VEC; ++e) acc[e] = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
+                        for (int e = 0; e < VEC; ++e) acc[e] = mac<T>(acc[e], vv[u], xv[u].v[e]);
                     vp += R * C;
                     cp += R * C;
                 };
@@ -958,7 +969,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                         for (int u = 0; u < U; ++u) {
                             if (j0 + u < len) {
 #pragma unroll
-                                for (int e = 0; e < VEC; ++e) acc[e] = O::add(acc[e], O::mul(vv[u], xv[u].v[e]));
+                                for (int e = 0; e < VEC; ++e) acc[e] = mac<T>(acc[e], vv[u], xv[u].v[e]);
                             }
                         }
                         vp += U * C;
