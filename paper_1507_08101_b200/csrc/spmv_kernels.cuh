@@ -740,7 +740,7 @@ constexpr std::size_t rows_smem_bytes() {
            128;
 }
 
-template <class T, int C, int W, int U, bool DOTS, bool PLAIN>
+template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED>
 __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
     spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
             // the epilogue's y (AXPBY) and z (CHAIN) rows of this tile: one bulk L2
             // prefetch each, a stage ahead of the consumers, so the epilogue reads
             // hit L2 instead of adding a dependent HBM round trip per tile
-            if (kPrefetchEpi && lane == 0 && (a.flags & (kFlagAxpby | kFlagChain))) {
+            if (kPrefetchEpi && !MAPPED && lane == 0 && (a.flags & (kFlagAxpby | kFlagChain))) {
                 const gidx r0 = tile_rg(t) * 32;
                 const gidx r1 = min(r0 + gidx(rows_per_tile), min(gidx(a.nrows), a.rg1 * 32));
                 auto span = [&](const T* base, gidx rs) {
@@ -991,13 +991,15 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                 }
                 continue;
             }
-            // fused epilogue (spmv_epilogue.hpp:12-36)
+            // fused epilogue (spmv_epilogue.hpp:12-36); a remote-part sweep writes the
+            // local rows its stored rows map to (row_map)
             if (row < row_end) {
-                const bool fin = !deferred(a.defer_mask, row);
+                const gidx orow = MAPPED ? gidx(__ldg(a.row_map + row)) : gidx(row);
+                const bool fin = !deferred(a.defer_mask, orow);
                 const int cb = sub * VEC;
-                T* yp = a.y + row * a.y_rs + cb;
+                T* yp = a.y + orow * a.y_rs + cb;
                 Vec<T, VEC> xs, yv, out;
-                if (need_x) xs = ld_x<T, VEC>(a.xs + row * a.xs_rs + cb);
+                if (need_x) xs = ld_x<T, VEC>(a.xs + orow * a.xs_rs + cb);
                 if (a.flags & kFlagAxpby) {
                     if constexpr (kYHint && VEC * sizeof(T) == 32)
                         yv = ld_vec_hint<T, VEC>(yp, ypol);
@@ -1014,7 +1016,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                     st_vec<T, VEC>(yp, out);
                 if (fin) {
                     if (a.flags & kFlagChain) {
-                        T* zp = a.z + row * a.z_rs + cb;
+                        T* zp = a.z + orow * a.z_rs + cb;
                         Vec<T, VEC> zv = ld_vec<T, VEC>(zp);
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) zv.v[e] = O::add(O::mul(a.delta, zv.v[e]), O::mul(a.eta, out.v[e]));
@@ -1244,10 +1246,10 @@ inline int rows_mode() {
     return mode;
 }
 
-template <class T, int C, int W, bool DOTS, bool PLAIN>
+template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false>
 LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     constexpr int U = rows_unroll<T, W, DOTS>();
-    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN>;
+    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
     static bool attr = [&] {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1280,7 +1282,7 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
         const int rm = rows_mode();
         const bool rows = rm != 0;
         const bool stride_ok = gidx(a.x_rs) * gidx(sizeof(T)) < (gidx(1) << 31);  // 32-bit byte stride
-        if (rows && stride_ok && kernel_mode() != 1 && a.row_map == nullptr) {
+        if (rows && stride_ok && kernel_mode() != 1) {
             // tiles of at least SK_RTILE_ROWS rows (several warp passes when a warp's
             // rows are few), as far as one stage holds them
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
@@ -1288,6 +1290,9 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
             int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
                                cap);
             while (a.sweep_brg > 0 && rgt > 1 && a.sweep_brg % rgt != 0) --rgt;  // tiles inside blocks
+            if (rgt >= 1 && a.row_map != nullptr)  // remote-part sweep of a distributed matrix
+                return dots ? launch_tma_rows<T, C, W, true, false, true>(a, rgt, rt, st)
+                            : launch_tma_rows<T, C, W, false, false, true>(a, rgt, rt, st);
             if (rgt >= 1) {
                 if (dots) return launch_tma_rows<T, C, W, true, false>(a, rgt, rt, st);
                 // plain y = A x: no flag, alpha == 1, no deferred rows
