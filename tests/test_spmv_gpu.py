@@ -304,3 +304,40 @@ def test_large_stencil_bitwise(sk, orc):
     assert np.array_equal(y.copy_out(), yo)
     sc = np.concatenate([np.sum(yo ** 2, 0), np.sum(np.abs(xv * yo), 0), np.sum(xv ** 2, 0)])
     assert dots_close(dots, do, sc)
+
+
+@pytest.mark.parametrize("w", [1, 4, 8, 16, 32])
+@pytest.mark.parametrize("C,sigma", [(32, 256), (8, 64), (4, 1)])
+def test_irregular_rows_all_paths(sk, orc, w, C, sigma):
+    """Rows of very different lengths (empty rows, a 3000-nonzero row, a dense block of
+    long rows): exercises tiles whose chunks overflow a shared-memory stage, the
+    row-length remainder paths and the fallback kernels; y must stay bit-identical."""
+    rng = np.random.default_rng(1000 * w + C)
+    n = 5000
+    lens = rng.integers(0, 12, n)
+    lens[17] = 0
+    lens[100] = 3000
+    lens[2000:2040] = 400
+    rows, cols, vals = [], [], []
+    rp = [0]
+    for r in range(n):
+        c = np.sort(rng.choice(n, size=int(lens[r]), replace=False))
+        cols.append(c)
+        vals.append(rng.uniform(-1, 1, len(c)))
+        rp.append(rp[-1] + len(c))
+    rp = np.array(rp, np.int64)
+    col = np.concatenate(cols).astype(np.int64)
+    val = np.concatenate(vals)
+    A = sk.crs(rp, col, val).build(C, sigma)
+    Ao = orc.build(rp, col, val, C, sigma)
+    xv = hash_block(n, w, 7)
+    y0 = hash_block(n, w, 8)
+    x, y = sk.densemat_from(xv), sk.densemat_from(y0)
+    flags = sellkit.AXPBY | sellkit.SHIFT
+    sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    yo, _, _ = orc.spmv(Ao, xv, y0, None, flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    assert np.array_equal(y.copy_out(), yo)
+    y2 = sk.densemat(n, w)
+    sk.spmv(y2, A, x)
+    yo2, _, _ = orc.spmv(Ao, xv)
+    assert np.array_equal(y2.copy_out(), yo2)
