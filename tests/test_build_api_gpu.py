@@ -1,0 +1,130 @@
+"""Construction and refresh entry points: matrices from the
+row callback (sellkit_crs_from_rowfunc / sellkit_mat_build_rowfunc), value refresh
+(sellkit_mat_update_values) and the CRS export (sellkit_mat_to_crs), checked like the
+reference's own tests (proj/tests/unit_sparse.cpp:155-246, unit_capi.cpp:64-110,225-245):
+layouts bit-identical to the CRS build, exact round trips, typed errors."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle.oracle import random_crs
+from paper_1507_08101_b200 import sellkit
+from paper_1507_08101_b200.sellkit import ROW_FN, SellkitError, vp
+
+pytestmark = pytest.mark.gpu
+
+LAYOUT = ["row_perm_inv", "row_perm", "rowlen", "chunk_len", "chunk_offset", "val", "col"]
+
+
+def _rowfn(rp, col, val, cap=None):
+    """ctypes row callback serving CRS rows (optionally writing at most `cap` entries)."""
+    def fn(row, lenp, cols, vals, _arg):
+        b, e = int(rp[row]), int(rp[row + 1])
+        lenp[0] = e - b
+        k = e - b if cap is None else min(e - b, cap)
+        vv = C.cast(vals, C.POINTER(C.c_double))
+        for j in range(k):
+            cols[j] = int(col[b + j])
+            vv[j] = float(val[b + j])
+        return 0
+    return ROW_FN(fn)
+
+
+def _gcrs(crs, path):
+    crs.write_bin(str(path))
+    return open(path, "rb").read()
+
+
+def _irregular(seed=3, n=700):
+    rng = np.random.default_rng(seed)
+    rp, col, val = random_crs(rng, n, n, 0.01)
+    return rp, col, val
+
+
+def test_rowfunc_build_matches_crs_build(sk, tmp_path):
+    rp, col, val = _irregular()
+    n = len(rp) - 1
+    maxlen = int(np.max(np.diff(rp)))
+    for C_, sigma in [(32, 256), (4, 8), (1, 1), (8, 1)]:
+        A = sk.crs(rp, col, val).build(C_, sigma)
+        cb = _rowfn(rp, col, val)
+        h = vp()
+        sk.call("sellkit_mat_build_rowfunc", sellkit.R64, n, n, maxlen, cb, None, C_, sigma, C.byref(h))
+        B = sellkit.Mat(sk, h, sellkit.R64)
+        la, lb = A.export(), B.export()
+        for key in LAYOUT:
+            assert np.array_equal(la[key], lb[key]), (C_, sigma, key)
+    # CRS from the callback == CRS from the arrays (byte-identical GCRS files)
+    cb = _rowfn(rp, col, val)
+    h = vp()
+    sk.call("sellkit_crs_from_rowfunc", sellkit.R64, n, n, maxlen, cb, None, C.byref(h))
+    assert _gcrs(sellkit.Crs(sk, h, sellkit.R64), tmp_path / "a.gcrs") == _gcrs(sk.crs(rp, col, val), tmp_path / "b.gcrs")
+    # a row longer than max_rowlen is rejected (the callback never writes past the capacity)
+    lying = _rowfn(rp, col, val, cap=maxlen - 1)
+    with pytest.raises(SellkitError) as ei:
+        sk.call("sellkit_mat_build_rowfunc", sellkit.R64, n, n, maxlen - 1, lying, None, 32, 256, C.byref(vp()))
+    assert ei.value.code == sellkit.ERR_INVALID_ARG
+
+
+def test_update_values_and_to_crs_round_trip(sk, tmp_path):
+    rp, col, val = _irregular(seed=5)
+    src = sk.crs(rp, col, val)
+    A = src.build(32, 256)
+    before = A.export()
+    # to_crs recovers the input exactly (unit_sparse.cpp:221-231)
+    h = vp()
+    sk.call("sellkit_mat_to_crs", A, C.byref(h))
+    back = sellkit.Crs(sk, h, sellkit.R64)
+    assert _gcrs(back, tmp_path / "back.gcrs") == _gcrs(src, tmp_path / "src.gcrs")
+    # update_values: layout untouched, values = those of a fresh build (unit_sparse.cpp:189-219)
+    doubled = sk.crs(rp, col, 2.0 * val)
+    sk.call("sellkit_mat_update_values", A, doubled)
+    after = A.export()
+    fresh = sk.crs(rp, col, 2.0 * val).build(32, 256).export()
+    for key in LAYOUT:
+        if key != "val":
+            assert np.array_equal(after[key], before[key]), key
+    assert np.array_equal(after["val"], fresh["val"])
+    again = after["val"].copy()
+    sk.call("sellkit_mat_update_values", A, doubled)
+    assert np.array_equal(A.export()["val"], again)  # idempotent
+    # one more nonzero: pattern mismatch
+    rp2 = rp.copy()
+    rp2[1:] += 1
+    col2 = np.insert(col, 0, 0 if col[0] != 0 else 1)
+    if rp[1] > 0:
+        seg = np.sort(col2[: rp2[1]])
+        col2[: rp2[1]] = seg
+    val2 = np.insert(val, 0, 1.0)
+    try:
+        extra = sk.crs(rp2, col2, val2)
+    except SellkitError:
+        pytest.skip("could not form the extra-nonzero matrix")
+    with pytest.raises(SellkitError) as ei:
+        sk.call("sellkit_mat_update_values", A, extra)
+    assert ei.value.code == sellkit.ERR_PATTERN
+
+
+def test_capi_identity_callback_and_empty_rows(sk, tmp_path):
+    """unit_capi.cpp:64-110 (diag(1..8) through the callback, <y,y> = 204) and the empty-row
+    round trip of unit_sparse.cpp:235-246."""
+    def diag(row, lenp, cols, vals, _arg):
+        lenp[0] = 1
+        cols[0] = row
+        C.cast(vals, C.POINTER(C.c_double))[0] = float(row + 1)
+        return 0
+    cb = ROW_FN(diag)
+    h = vp()
+    sk.call("sellkit_crs_from_rowfunc", sellkit.R64, 8, 8, 1, cb, None, C.byref(h))
+    A = sellkit.Crs(sk, h, sellkit.R64).build(4, 4)
+    assert A.stats()[0] == 1.0
+    x, y = sk.densemat_from(np.ones((8, 1))), sk.densemat(8, 1)
+    d = np.zeros(3)
+    sk.spmv(y, A, x, flags=sellkit.DOT_YY, dot=d)
+    assert d[0] == 204.0 and y.copy_out().sum() == 36.0
+    gaps = sk.crs(np.array([0, 1, 1, 2]), np.array([0, 2]), np.array([1.0, 2.0]))
+    G = gaps.build(2, 1)
+    h = vp()
+    sk.call("sellkit_mat_to_crs", G, C.byref(h))
+    assert _gcrs(sellkit.Crs(sk, h, sellkit.R64), tmp_path / "g.gcrs") == _gcrs(gaps, tmp_path / "g0.gcrs")
