@@ -158,3 +158,37 @@ def test_pencil_order_is_a_block_permutation():
     import pytest
     with pytest.raises(ValueError):
         pencil_order(10, 4, 4, per_site=1, block_rows=32)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                    "oracle", "_ref", "libsellkit.so")),
+                    reason="oracle/_ref not built")
+def test_perf_model_equals_reference_library(sk):
+    """Host-side perf model (perfmodel.cpp:11-45) against the reference library itself
+    (oracle/_ref) over a grid of inputs: identical doubles and error codes."""
+    from oracle.oracle import REF_LIB_PATH
+    ref = C.CDLL(REF_LIB_PATH)
+    ref.sellkit_spmv_code_balance.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_double)]
+    ref.sellkit_roofline_bound.argtypes = [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]
+    ref.sellkit_crs_refresh_cost.argtypes = [C.c_int64, C.c_int, C.c_double, C.POINTER(C.c_double)]
+    ref.sellkit_index_width_saving.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    a, b = C.c_double(), C.c_double()
+    for dt in (sellkit.R32, sellkit.R64, sellkit.C32, sellkit.C64):
+        for ib in (2, 4, 8, 3):
+            for vec in (0, 1):
+                for nnzr in (0.0, 1.0, 7.0, 13.5):
+                    e1 = sk.lib.sellkit_spmv_code_balance(dt, ib, vec, nnzr, C.byref(a))
+                    e2 = ref.sellkit_spmv_code_balance(dt, ib, vec, nnzr, C.byref(b))
+                    assert e1 == e2 and (e1 != 0 or a.value == b.value), (dt, ib, vec, nnzr)
+    for bw, pk, cb in [(50.0, 176.0, 6.0), (6465.8, 37000.0, 1.895), (1.0, 1.0, 0.0), (-1.0, 2.0, 3.0)]:
+        e1 = sk.lib.sellkit_roofline_bound(bw, pk, cb, C.byref(a))
+        e2 = ref.sellkit_roofline_bound(bw, pk, cb, C.byref(b))
+        assert e1 == e2 and (e1 != 0 or a.value == b.value)
+    for nnz, vb, bw in [(100, 8, 1200.0), (447040000, 8, 6465.8), (0, 16, 1.0), (5, 3, 2.0)]:
+        e1 = sk.lib.sellkit_crs_refresh_cost(nnz, vb, bw, C.byref(a))
+        e2 = ref.sellkit_crs_refresh_cost(nnz, vb, bw, C.byref(b))
+        assert e1 == e2 and (e1 != 0 or a.value == b.value)
+    for vb in (1, 2, 4, 8, 16, 7):
+        e1 = sk.lib.sellkit_index_width_saving(vb, C.byref(a))
+        e2 = ref.sellkit_index_width_saving(vb, C.byref(b))
+        assert e1 == e2 and (e1 != 0 or a.value == b.value)
