@@ -300,15 +300,19 @@ def run_ours(args, rank, world, local_rank):
         e0.record(stream)
         for _ in range(args.e2e_steps):
             e2e_step()
+        if job is not None and job.e2e_flush is not None:
+            job.e2e_flush()
         e1.record(stream)
         torch.cuda.synchronize()
+        sk.set_sync(True)
         te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device="cuda")
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": flops_step / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": float(te.item()), "steps": args.e2e_steps,
                "path": ("sellkit_spmv on view_plain host buffers (pinned), streamed H2D/sweep/D2H"
-                        if job is None else "copy_in + sellkit_ext_rank_spmv + copy_out per rank")}
+                        if job is None else "per rank: H2D x, sellkit_ext_rank_spmv, D2H y; consecutive steps "
+                        "overlap the upload with the previous download")}
 
     if rank != 0:
         return

@@ -291,6 +291,7 @@ class BenchJob:
     h2d_bytes: int
     d2h_bytes: int
     keep: list = field(default_factory=list)
+    e2e_flush: Optional[Callable[[], None]] = None
 
     def kernel_ms(self, per_step: List[float]) -> float:
         return float(np.mean(per_step))
@@ -307,9 +308,13 @@ def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank
     rc = setup_rank(sk, rows, off, rank, world, chunk_height, sigma)
     del rows
     nloc = r1 - r0
-    x = sk.densemat(nloc, w)
+    # rank vectors in HBM (torch allocations viewed by the library: the e2e copies below
+    # run on torch copy streams)
+    xt = torch.empty((nloc, w), dtype=torch.float64, device="cuda")
+    yt = torch.empty((nloc, w), dtype=torch.float64, device="cuda")
+    x = sk.view_plain(xt.data_ptr(), nloc * w, nloc, w, w, keep=xt)
+    y = sk.view_plain(yt.data_ptr(), nloc * w, nloc, w, w, keep=yt)
     x.fill_hash(42 + rank)
-    y = sk.densemat(nloc, w)
     st = rc.stats()
     opts = sellkit.spmv_opts()
     sk.lib.sellkit_spmv_opts_init(C.byref(opts))
@@ -319,12 +324,33 @@ def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank
 
     xh = torch.empty((nloc, w), dtype=torch.float64, pin_memory=True)
     yh = torch.empty((nloc, w), dtype=torch.float64, pin_memory=True)
-    sk.call("sellkit_densemat_copy_out", x.h, vp(xh.data_ptr()), nloc * w)
+    xh.copy_(xt)
+
+    # e2e step: H2D of x (copy stream), the distributed sweep (library stream), D2H of y
+    # (second copy stream).  Consecutive steps pipeline: step i+1's x upload overlaps
+    # step i's y download (the two directions of the link); the sweep waits for its x and
+    # for the previous download to release y.
+    lib = torch.cuda.ExternalStream(sk.stream())
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_x, ev_sweep, ev_y = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
 
     def e2e_step():
-        sk.call("sellkit_densemat_copy_in", x.h, vp(xh.data_ptr()), nloc * w)
+        s_in.wait_event(ev_sweep)           # previous sweep finished reading x
+        with torch.cuda.stream(s_in):
+            xt.copy_(xh, non_blocking=True)
+            ev_x.record(s_in)
+        lib.wait_event(ev_x)
+        lib.wait_event(ev_y)                # previous download finished reading y
+        sk.set_sync(False)
         step()
-        sk.call("sellkit_densemat_copy_out", y.h, vp(yh.data_ptr()), nloc * w)
+        ev_sweep.record(lib)
+        s_out.wait_event(ev_sweep)
+        with torch.cuda.stream(s_out):
+            yh.copy_(yt, non_blocking=True)
+            ev_y.record(s_out)
+
+    def e2e_flush():
+        lib.wait_event(ev_y)                # the timed region ends after the last download
 
     # our kernels per step: pack (one per send list) + local sweep + remote sweep; the stencil
     # coupling is symmetric, so we send to exactly the owners we receive from
@@ -333,7 +359,7 @@ def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank
     halo_bytes = st["n_halo"] * w * 8
     return BenchJob(step=step, e2e_step=e2e_step, rows_local=nloc, nnz_local=nnz_local, halo_bytes=halo_bytes,
                     launches_per_step=launches, h2d_bytes=nloc * w * 8, d2h_bytes=nloc * w * 8,
-                    keep=[rc, x, y, xh, yh, opts])
+                    keep=[rc, x, y, xt, yt, xh, yh, opts, s_in, s_out], e2e_flush=e2e_flush)
 
 
 # ------------------------------------------------------- tall-skinny, sharded
