@@ -88,12 +88,12 @@ struct MmGeom {
     static constexpr int CN = KB < 4 ? KB : 4;
     static constexpr int WPR = KB / CN;           // warps per row set
     static constexpr int RSETS = 8 / WPR;         // row sets per CTA
-    static constexpr int RM = SK_MM_RM;           // 8-row blocks per warp
+    static constexpr int RM = KB >= 8 ? SK_MM_RM : 1;  // 8-row blocks per warp (1 for k <= 32: more CTAs)
     static constexpr int RB = RSETS * RM * 8;     // rows per tile
 };
 
 template <int KB>
-__global__ void __launch_bounds__(kMT, SK_MM_MINB)
+__global__ void __launch_bounds__(kMT, KB >= 8 ? SK_MM_MINB : SK_MM_MINB + 1)
     tsmm_dmma_kernel(double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ xcm, gidx n,
                      int m, double alpha, double beta, int beta_zero) {
     using G = MmGeom<KB>;
