@@ -113,7 +113,10 @@ DeviceRuntime& runtime(int device) {
     auto* rt = new DeviceRuntime();
     rt->device = device;
     DeviceGuard g(device);
-    CK(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking));
+    // A *blocking* stream: work the caller queued on the legacy default stream (e.g. torch
+    // filling a buffer passed through view_plain) completes before the library reads it,
+    // and vice versa -- the reference API's synchronous semantics for device pointers.
+    CK(cudaStreamCreateWithFlags(&rt->stream, cudaStreamDefault));
     CK(cudaDeviceGetAttribute(&rt->num_sms, cudaDevAttrMultiProcessorCount, device));
     int l2 = 0;
     CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
