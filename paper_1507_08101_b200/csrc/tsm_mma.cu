@@ -42,6 +42,9 @@ constexpr int kMT = 256;  // threads per CTA (8 warps)
 #ifndef SK_MM_MINB
 #define SK_MM_MINB 3
 #endif
+#ifndef SK_TT_AM
+#define SK_TT_AM 2
+#endif
 #ifndef SK_TT_MINB
 #define SK_TT_MINB 2
 #endif
@@ -170,9 +173,14 @@ __global__ void __launch_bounds__(kMT, KB >= 8 ? SK_MM_MINB : SK_MM_MINB + 1)
 template <int MB, int KB>
 struct TtGeom {
     static constexpr int NBLK = MB * KB;
-    static constexpr int BPW = NBLK >= 8 ? NBLK / 8 : 1;   // blocks per warp (same a-block, consecutive b)
+    static constexpr int BPW = NBLK >= 8 ? NBLK / 8 : 1;   // blocks per warp
     static constexpr int RS = NBLK >= 8 ? 1 : 8 / NBLK;    // row splits (warps sharing a block set)
     static constexpr int RB = SK_TT_RB;                     // rows per tile
+    // a warp owns an AM x BN rectangle of blocks: per row quad it loads AM A- and BN
+    // B-fragments for AM * BN DMMAs (2 x 4: 6 LDS per 8 DMMA instead of 9 for 1 x 8)
+    static constexpr int AM = (SK_TT_AM > 1 && BPW >= 4 && MB % 2 == 0) ? 2 : 1;
+    static constexpr int BN = BPW / AM;
+    static_assert(KB % BN == 0 && MB % AM == 0, "block rectangle must tile the result");
 };
 
 template <int MB, int KB>
@@ -185,17 +193,19 @@ __global__ void __launch_bounds__(kMT, SK_TT_MINB)
     extern __shared__ __align__(16) double sm[];
     double* vt = sm;                        // 2 x RB x pv
     double* wt = vt + 2 * G::RB * pv;       // 2 x RB x pw
-    double* red = wt + 2 * G::RB * pw;      // [8 warps][BPW blocks][64]
+    double* red = wt + 2 * G::RB * pw;      // [RS][NBLK][64] (= 8 x BPW x 64)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rs = warp % G::RS, bg = warp / G::RS;
-    const int q0 = bg * G::BPW;                  // first block of this warp
-    const int ab = q0 / KB, bb0 = q0 - ab * KB;  // a-block, first b-block
+    constexpr int NCG = KB / G::BN;                        // column groups of blocks
+    const int ab0 = (bg / NCG) * G::AM, bb0 = (bg % NCG) * G::BN;  // first a-block, b-block
     const gidx r0 = gidx(blockIdx.x) * rows_per_cta;
     const gidx r1 = min(n, r0 + rows_per_cta);
     const gidx ntiles = r1 > r0 ? (r1 - r0 + G::RB - 1) / G::RB : 0;
-    double acc[G::BPW][2];
+    double acc[G::AM][G::BN][2];
 #pragma unroll
-    for (int j = 0; j < G::BPW; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int i = 0; i < G::AM; ++i)
+#pragma unroll
+        for (int j = 0; j < G::BN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     auto stage = [&](gidx tile, int s) {
         const gidx rb = r0 + tile * G::RB;
         const int nr = int(min(gidx(G::RB), r1 - rb));
@@ -214,16 +224,19 @@ __global__ void __launch_bounds__(kMT, SK_TT_MINB)
         const double* vs = vt + (t & 1) * G::RB * pv;
         const double* ws = wt + (t & 1) * G::RB * pw;
         // A (8 a x 4 rows): lane -> V[row + l%4][a + l/4]; B (4 rows x 8 b): W[row + l%4][b + l/4]
-        const double* ap = vs + (lane & 3) * pv + ab * 8 + (lane >> 2);
+        const double* ap = vs + (lane & 3) * pv + ab0 * 8 + (lane >> 2);
         const double* bp = ws + (lane & 3) * pw + bb0 * 8 + (lane >> 2);
 #pragma unroll 4
         for (int r4 = rs; r4 < G::RB / 4; r4 += G::RS) {
-            const double a = ap[r4 * 4 * pv];
-            double b[G::BPW];
+            double a[G::AM], b[G::BN];
 #pragma unroll
-            for (int j = 0; j < G::BPW; ++j) b[j] = bp[r4 * 4 * pw + j * 8];
+            for (int i = 0; i < G::AM; ++i) a[i] = ap[r4 * 4 * pv + i * 8];
 #pragma unroll
-            for (int j = 0; j < G::BPW; ++j) dmma(acc[j][0], acc[j][1], a, b[j]);
+            for (int j = 0; j < G::BN; ++j) b[j] = bp[r4 * 4 * pw + j * 8];
+#pragma unroll
+            for (int i = 0; i < G::AM; ++i)
+#pragma unroll
+                for (int j = 0; j < G::BN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
         __syncthreads();
     }
@@ -231,19 +244,21 @@ __global__ void __launch_bounds__(kMT, SK_TT_MINB)
     // warp partials -> shared memory, then the row splits of each block are summed
     // in a fixed order and written col-major (cell = b*m + a, as tsm.hpp:145)
 #pragma unroll
-    for (int j = 0; j < G::BPW; ++j) {
-        red[(warp * G::BPW + j) * 64 + lane * 2] = acc[j][0];
-        red[(warp * G::BPW + j) * 64 + lane * 2 + 1] = acc[j][1];
-    }
+    for (int i = 0; i < G::AM; ++i)
+#pragma unroll
+        for (int j = 0; j < G::BN; ++j) {
+            const int blk = (ab0 + i) * KB + bb0 + j;
+            red[(rs * G::NBLK + blk) * 64 + lane * 2] = acc[i][j][0];
+            red[(rs * G::NBLK + blk) * 64 + lane * 2 + 1] = acc[i][j][1];
+        }
     __syncthreads();
     for (int c = threadIdx.x; c < m * k; c += kMT) {
         const int a = c % m, b = c / m;
         const int blk = (a / 8) * KB + b / 8;
-        const int bgx = blk / G::BPW, j = blk - bgx * G::BPW;
         // fragment position of (a % 8, b % 8): lane = (a%8)*4 + (b%8)/2, element (b%8)%2
         const int idx = ((a & 7) * 4 + ((b & 7) >> 1)) * 2 + (b & 1);
         double s = 0.0;
-        for (int q = 0; q < G::RS; ++q) s = __dadd_rn(s, red[((bgx * G::RS + q) * G::BPW + j) * 64 + idx]);
+        for (int q = 0; q < G::RS; ++q) s = __dadd_rn(s, red[(q * G::NBLK + blk) * 64 + idx]);
         partial[gidx(blockIdx.x) * m * k + c] = s;
     }
 }
