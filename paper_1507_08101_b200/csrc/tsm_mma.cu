@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "ops.cuh"
+#include "tma.cuh"
 #include "tsm.cuh"
 
 namespace skb {
@@ -41,6 +42,19 @@ constexpr int kMT = 256;  // threads per CTA (8 warps)
 #endif
 #ifndef SK_MM_MINB
 #define SK_MM_MINB 3
+#endif
+// V row tiles of the compute-bound TSMM shapes (k, m >= 32) staged by per-row bulk
+// copies (one warp, mbarrier-completed) instead of 16-B cp.async from every thread:
+// the staging address math left the DMMA pipe idle (m = k = 64, N = 1e8: 30.4 ->
+// 27.3 ms).  The bandwidth-bound small shapes keep cp.async (short rows are
+// slow bulk copies: m = k = 16 3.9 -> 5.5 ms).
+#ifndef SK_MM_BULK
+#define SK_MM_BULK 1
+#endif
+// The same staging for TSMTTSM (V and W rows, zeroed short tiles) is slower with its
+// 32-row tiles (m = k = 64: 26.9 -> 31.8 ms; 32: 9.2 -> 12.6 ms): off
+#ifndef SK_TT_BULK
+#define SK_TT_BULK 0
 #endif
 #ifndef SK_TT_AM
 #define SK_TT_AM 2
@@ -95,7 +109,7 @@ struct MmGeom {
     static constexpr int RB = RSETS * RM * 8;     // rows per tile
 };
 
-template <int KB>
+template <int KB, bool BULK>
 __global__ void __launch_bounds__(kMT, KB >= 8 ? SK_MM_MINB : SK_MM_MINB + 1)
     tsmm_dmma_kernel(double* __restrict__ w, const double* __restrict__ v, const double* __restrict__ xcm, gidx n,
                      int m, double alpha, double beta, int beta_zero) {
@@ -115,14 +129,42 @@ __global__ void __launch_bounds__(kMT, KB >= 8 ? SK_MM_MINB : SK_MM_MINB + 1)
     const int rset = warp / G::WPR, cset = warp - rset * G::WPR;
     const int rbase = rset * G::RM * 8, cb0 = cset * G::CN;
     gidx t = blockIdx.x;
-    if (t < ntiles) stage_rows(vt, v, n, t * G::RB, G::RB, m, ps);
-    cp_commit();
+    __shared__ __align__(8) std::uint64_t full[2];
+    const unsigned long long pol = l2_evict_first_policy();
+    // BULK: rows past n are not copied; their (stale) products are never stored
+    auto issue = [&](gidx tile, int s) {
+        if constexpr (BULK) {
+            if (warp != 0) return;
+            const gidx rb = tile * G::RB;
+            const int nr = int(min(gidx(G::RB), n - rb));
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], std::uint32_t(nr) * std::uint32_t(m) * 8u);
+            __syncwarp();
+            for (int r = lane; r < nr; r += 32)
+                bulk_g2s(vt + (s * G::RB + r) * ps, v + (rb + r) * m, std::uint32_t(m) * 8u, &full[s], pol);
+        } else {
+            stage_rows(vt + s * G::RB * ps, v, n, tile * G::RB, G::RB, m, ps);
+        }
+    };
+    if constexpr (BULK) {
+        if (threadIdx.x == 0) {
+            mbar_init(&full[0], 1);
+            mbar_init(&full[1], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    }
+    if (t < ntiles) issue(t, 0);
+    if constexpr (!BULK) cp_commit();
     for (int it = 0; t < ntiles; ++it, t += gridDim.x) {
         const gidx tn = t + gridDim.x;
-        if (tn < ntiles) stage_rows(vt + ((it + 1) & 1) * G::RB * ps, v, n, tn * G::RB, G::RB, m, ps);
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
+        if (tn < ntiles) issue(tn, (it + 1) & 1);
+        if constexpr (BULK) {
+            mbar_wait(&full[it & 1], std::uint32_t(it >> 1) & 1u);
+        } else {
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+        }
         const double* vs = vt + (it & 1) * G::RB * ps;
         double acc[G::RM][G::CN][2];
 #pragma unroll
@@ -166,7 +208,7 @@ __global__ void __launch_bounds__(kMT, KB >= 8 ? SK_MM_MINB : SK_MM_MINB + 1)
         }
         __syncthreads();  // this stage is refilled two iterations on
     }
-    cp_wait<0>();
+    if constexpr (!BULK) cp_wait<0>();
 }
 
 // --------------------------------------------------------------- TSMTTSM ----
@@ -183,7 +225,7 @@ struct TtGeom {
     static_assert(KB % BN == 0 && MB % AM == 0, "block rectangle must tile the result");
 };
 
-template <int MB, int KB>
+template <int MB, int KB, bool BULK>
 __global__ void __launch_bounds__(kMT, SK_TT_MINB)
     tsmttsm_dmma_kernel(const double* __restrict__ v, const double* __restrict__ w, gidx n, gidx rows_per_cta,
                         double* __restrict__ partial) {
@@ -206,21 +248,54 @@ __global__ void __launch_bounds__(kMT, SK_TT_MINB)
     for (int i = 0; i < G::AM; ++i)
 #pragma unroll
         for (int j = 0; j < G::BN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    __shared__ __align__(8) std::uint64_t full[2];
+    const unsigned long long pol = l2_evict_first_policy();
     auto stage = [&](gidx tile, int s) {
         const gidx rb = r0 + tile * G::RB;
-        const int nr = int(min(gidx(G::RB), r1 - rb));
-        // rows past r1 are zero-filled (n argument = r1)
-        stage_rows(vt + s * G::RB * pv, v, r1, rb, G::RB, m, pv);
-        stage_rows(wt + s * G::RB * pw, w, r1, rb, G::RB, k, pw);
-        (void)nr;
+        if constexpr (BULK) {
+            // rows [nr, RB) of a short last tile are zeroed (they enter the row sum);
+            // the trailing __syncthreads of the iteration publishes the zeros
+            const int nr = int(min(gidx(G::RB), r1 - rb));
+            if (nr < G::RB) {
+                for (int q = threadIdx.x; q < (G::RB - nr) * pv; q += kMT) vt[(s * G::RB + nr) * pv + q] = 0.0;
+                for (int q = threadIdx.x; q < (G::RB - nr) * pw; q += kMT) wt[(s * G::RB + nr) * pw + q] = 0.0;
+            }
+            if (warp != 0) return;
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], std::uint32_t(nr) * std::uint32_t(m + k) * 8u);
+            __syncwarp();
+            for (int r = lane; r < nr; r += 32) {
+                bulk_g2s(vt + (s * G::RB + r) * pv, v + (rb + r) * m, m * 8u, &full[s], pol);
+                bulk_g2s(wt + (s * G::RB + r) * pw, w + (rb + r) * k, k * 8u, &full[s], pol);
+            }
+        } else {
+            // rows past r1 are zero-filled (n argument = r1)
+            stage_rows(vt + s * G::RB * pv, v, r1, rb, G::RB, m, pv);
+            stage_rows(wt + s * G::RB * pw, w, r1, rb, G::RB, k, pw);
+        }
     };
+    if constexpr (BULK) {
+        if (threadIdx.x == 0) {
+            mbar_init(&full[0], 1);
+            mbar_init(&full[1], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    }
     if (ntiles > 0) stage(0, 0);
-    cp_commit();
+    if constexpr (BULK) {
+        __syncthreads();  // zero rows of a one-tile range
+    } else {
+        cp_commit();
+    }
     for (gidx t = 0; t < ntiles; ++t) {
         if (t + 1 < ntiles) stage(t + 1, int((t + 1) & 1));
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
+        if constexpr (BULK) {
+            mbar_wait(&full[t & 1], std::uint32_t(t >> 1) & 1u);
+        } else {
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+        }
         const double* vs = vt + (t & 1) * G::RB * pv;
         const double* ws = wt + (t & 1) * G::RB * pw;
         // A (8 a x 4 rows): lane -> V[row + l%4][a + l/4]; B (4 rows x 8 b): W[row + l%4][b + l/4]
@@ -240,7 +315,7 @@ __global__ void __launch_bounds__(kMT, SK_TT_MINB)
         }
         __syncthreads();
     }
-    cp_wait<0>();
+    if constexpr (!BULK) cp_wait<0>();
     // warp partials -> shared memory, then the row splits of each block are summed
     // in a fixed order and written col-major (cell = b*m + a, as tsm.hpp:145)
 #pragma unroll
@@ -285,7 +360,8 @@ bool tsmm_dmma(double* w, const double* v, const double* xcm, gidx n, int m, int
         using G = MmGeom<KB>;
         const std::size_t smem = (std::size_t(m) * KB * 8 + 2 * std::size_t(G::RB) * pitch_of(m)) * sizeof(double);
         if (smem > 220 * 1024) return;
-        auto kern = tsmm_dmma_kernel<KB>;
+        const bool bulk = SK_MM_BULK && KB >= 4 && m >= 32;
+        auto kern = bulk ? tsmm_dmma_kernel<KB, true> : tsmm_dmma_kernel<KB, false>;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const gidx ntiles = (n + G::RB - 1) / G::RB;
         int per_sm = 0;
@@ -309,7 +385,8 @@ int tsmttsm_dmma_partials(const double* v, const double* w, gidx n, int m, int k
             const std::size_t smem =
                 (2 * std::size_t(G::RB) * (pitch_of(MB * 8) + pitch_of(KB * 8)) + 8 * std::size_t(G::BPW) * 64) *
                 sizeof(double);
-            auto kern = tsmttsm_dmma_kernel<MB, KB>;
+            const bool bulk = SK_TT_BULK && MB >= 4 && KB >= 4;
+            auto kern = bulk ? tsmttsm_dmma_kernel<MB, KB, true> : tsmttsm_dmma_kernel<MB, KB, false>;
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             int per_sm = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMT, smem));

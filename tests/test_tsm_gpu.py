@@ -178,3 +178,19 @@ def test_sharded_tsm_wrappers_single_rank(sk, orc):
     xs = sk.densemat_from(X[:m, :k])
     dist.tsmm(sk, w2, v, xs, alpha=1.5, beta=-0.5)
     assert np.max(np.abs(w2.copy_out() - (1.5 * V @ X - 0.5 * W)) / (1 + np.abs(W))) < 1e-12
+
+
+@pytest.mark.parametrize("m,k", [(32, 32), (64, 64), (32, 64), (64, 32), (16, 64)])
+@pytest.mark.parametrize("n", [5, 1001, 70001])
+def test_tsm_tensor_core_ragged_rows(sk, orc, m, k, n):
+    # DMMA kernels with bulk-copied row tiles: short last tiles, one-tile ranges
+    rng = np.random.default_rng(n + m * 7 + k)
+    V, W, X = rng.uniform(-1, 1, (n, m)), rng.uniform(-1, 1, (n, k)), rng.uniform(-1, 1, (m, k))
+    want = orc.tsmttsm(V, W, X, 1.25, -0.5) if n < 5000 else 1.25 * (V.T @ W) - 0.5 * X
+    got = run_tsmttsm(sk, V, W, X, 1.25, -0.5)
+    scale = np.abs(V).T @ np.abs(W)
+    assert np.all(np.abs(got - want) <= 1e-12 * (1 + scale + np.abs(X)))
+    W0 = rng.uniform(-1, 1, (n, k))
+    want = orc.tsmm(V, X, W0, 1.5, 0.0) if n < 5000 else 1.5 * (V @ X)
+    got = run_tsmm(sk, V, X, W0, 1.5, 0.0)
+    assert np.max(np.abs(got - want) / (1 + np.abs(V) @ np.abs(X))) < 1e-12
