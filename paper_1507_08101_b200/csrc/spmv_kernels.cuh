@@ -657,6 +657,36 @@ __device__ __forceinline__ void slot_add(T* p, T v) {
 #ifndef SK_TAILMODE
 #define SK_TAILMODE 0
 #endif
+// Warp-uniform rows of length <= SK_LENSWITCH run a fully unrolled batch sequence
+// selected by the length (no trip-count arithmetic or loop); 0 = off.  Dots-free
+// kernels with w <= 16 only.  Measured (400^3, same box, ms): w = 1 0.976 -> 0.948,
+// w = 4 1.425 -> 1.390, w = 16 4.9 -> 4.5, bench w = 8 (power-capped, 200 steps)
+// 2.57 -> 2.525; w = 32 9.2 -> 9.8 and the dots kernels (C3 C64 5.84 -> 7.59) got
+// worse schedules, so they keep the loop.
+#ifndef SK_LENSWITCH
+#define SK_LENSWITCH 8
+#endif
+
+// f(integral_constant<U>) L / U times, then f(integral_constant<L % U>)
+template <int L, int U, class F>
+__device__ __forceinline__ void fixed_batches(F& f) {
+    if constexpr (L >= U) {
+        f(std::integral_constant<int, U>{});
+        fixed_batches<L - U, U>(f);
+    } else if constexpr (L > 0) {
+        f(std::integral_constant<int, L>{});
+    }
+}
+
+template <int LMAX, int U, class F>
+__device__ __forceinline__ void len_dispatch(int len, F& f) {
+    if constexpr (LMAX >= 1) {
+        if (len == LMAX)
+            fixed_batches<LMAX, U>(f);
+        else
+            len_dispatch<LMAX - 1, U>(len, f);
+    }
+}
 
 // acc + v * x: two separately rounded operations (the reference's arithmetic, bit-exact)
 // or, with SK_SPMV_FMA, one fused multiply-add (within the 1e-12 tolerance).
@@ -929,6 +959,12 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
                     cp += R * C;
                 };
                 lidx j0 = 0;
+                if constexpr (SK_LENSWITCH > 0 && SK_TAILMODE == 0 && !DOTS && W <= 16) {
+                    if (minlen == maxlen && len <= SK_LENSWITCH) {
+                        len_dispatch<SK_LENSWITCH, U>(len, batch);
+                        return;
+                    }
+                }
 #if SK_BATCH_UNROLL1
 #pragma unroll 1
 #endif
