@@ -259,6 +259,12 @@ __device__ __forceinline__ void store_row(T* p, const T (&r)[N]) {
     }
 }
 
+// TSMTTSM shapes with at least this many cells (and m, k multiples of 8) use DMMA
+// (m = k = 8 through DMMA measured 2.40 -> 2.37 ms at N = 1e8, within the spread: kept
+// on the register kernel)
+#ifndef SK_TT_DMMA_MIN_CELLS
+#define SK_TT_DMMA_MIN_CELLS 65
+#endif
 #ifndef SK_TT_UR_MAX
 #define SK_TT_UR_MAX 8
 #endif
@@ -575,7 +581,7 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
                 const gidx vst = vs.dev.stride, wst = wsg.dev.stride;
                 int used = 0;
                 if constexpr (std::is_same_v<T, double>) {
-                    if (!kahan && cells > 64 && vst == m && wst == k)
+                    if (!kahan && cells >= SK_TT_DMMA_MIN_CELLS && vst == m && wst == k)
                         used = tsmttsm_dmma_partials(vp, wp, n, m, k, p, nparts, rt);
                 }
                 if (used > 0) {
