@@ -265,6 +265,11 @@ __device__ __forceinline__ void store_row(T* p, const T (&r)[N]) {
 #ifndef SK_TT_DMMA_MIN_CELLS
 #define SK_TT_DMMA_MIN_CELLS 65
 #endif
+// partials (CTAs) per SM of the register TSMTTSM for m * k <= 4 (measured m = k = 1,
+// N = 1e8: 2 / 3 / 4 / 8 / 16 per SM -> 0.45 / 0.35 / 0.31 / 0.34 / 0.41 ms)
+#ifndef SK_TT_PARTS_SMALL
+#define SK_TT_PARTS_SMALL 4
+#endif
 #ifndef SK_TT_UR_MAX
 #define SK_TT_UR_MAX 8
 #endif
@@ -566,7 +571,7 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
     const gidx cells = gidx(m) * k;
     const std::size_t es = x.esize();
     if (!is_complex(x.dt) && compact_rows(vs.dev) && compact_rows(wsg.dev) && n > 0) {
-        const int nparts = int(std::max<gidx>(1, std::min<gidx>(gidx(rt.num_sms) * 4, (n + 255) / 256)));
+        const int nparts = int(std::max<gidx>(1, std::min<gidx>(gidx(rt.num_sms) * (cells <= 4 ? SK_TT_PARTS_SMALL : 4), (n + 255) / 256)));
         const gidx rows_per = (n + nparts - 1) / nparts;
         auto* part = static_cast<unsigned char*>(rt.scratch_bytes(std::size_t(nparts) * cells * es * 2 + 256));
         DAcc xa = dacc(xs.dev);
