@@ -727,6 +727,12 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 #ifndef SK_RMINB_DOTS
 #define SK_RMINB_DOTS 3
 #endif
+// the dots kernel of a single double vector fits 56 registers without spills: 4 CTAs/SM
+// (400^3 with three dots: w = 1 1.155 -> 1.055 ms; w = 2 1.40 -> 1.43, w = 4 1.89 ->
+// 1.88; wider blocks and complex/float types spill at 4 and lose 10-45 %)
+#ifndef SK_RMINB_DOTS_NARROW
+#define SK_RMINB_DOTS_NARROW 4
+#endif
 #ifndef SK_RSTAGES_WIDE
 #define SK_RSTAGES_WIDE 3
 #endif
@@ -771,7 +777,9 @@ constexpr std::size_t rows_smem_bytes() {
 }
 
 template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED>
-__global__ void __launch_bounds__(kTmaThreads, DOTS ? SK_RMINB_DOTS : SK_RMINB)
+__global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double> && W == 1 ? SK_RMINB_DOTS_NARROW
+                                                                                         : SK_RMINB_DOTS)
+                                                    : SK_RMINB)
     spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
     using P = RPlan<T, W>;
