@@ -678,13 +678,37 @@ __device__ __forceinline__ void fixed_batches(F& f) {
     }
 }
 
+// L split into ceil(L / U) batches of near-equal size, the larger ones first
+// (7 with U = 3: 3, 2, 2 instead of 3, 3, 1)
+template <int L, int NB, class F>
+__device__ __forceinline__ void balanced_batches(F& f) {
+    if constexpr (NB >= 1 && L > 0) {
+        constexpr int R = (L + NB - 1) / NB;
+        f(std::integral_constant<int, R>{});
+        balanced_batches<L - R, NB - 1>(f);
+    }
+}
+
+// Batch shape of the length-switched path: SK_LEN_UADD widens a batch beyond the
+// kernel's U, SK_LEN_BAL = 1 splits a row into near-equal batches instead of U-greedy ones.
+#ifndef SK_LEN_UADD
+#define SK_LEN_UADD 0
+#endif
+#ifndef SK_LEN_BAL
+#define SK_LEN_BAL 0
+#endif
+
 template <int LMAX, int U, class F>
 __device__ __forceinline__ void len_dispatch(int len, F& f) {
     if constexpr (LMAX >= 1) {
-        if (len == LMAX)
-            fixed_batches<LMAX, U>(f);
-        else
+        if (len == LMAX) {
+            if constexpr (SK_LEN_BAL)
+                balanced_batches<LMAX, (LMAX + U - 1) / U>(f);
+            else
+                fixed_batches<LMAX, U>(f);
+        } else {
             len_dispatch<LMAX - 1, U>(len, f);
+        }
     }
 }
 
@@ -969,7 +993,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 lidx j0 = 0;
                 if constexpr (SK_LENSWITCH > 0 && SK_TAILMODE == 0 && !DOTS && W <= 16) {
                     if (minlen == maxlen && len <= SK_LENSWITCH) {
-                        len_dispatch<SK_LENSWITCH, U>(len, batch);
+                        len_dispatch<SK_LENSWITCH, U + SK_LEN_UADD>(len, batch);
                         return;
                     }
                 }
