@@ -116,6 +116,23 @@ __device__ __forceinline__ bool deferred(const std::uint32_t* mask, gidx row) {
     return mask && ((mask[row >> 5] >> (row & 31)) & 1u);
 }
 
+// Producer look-ahead: after issuing tile it's copies, prefetch into L2 the chunk
+// headers (chunk_offset / chunk_len) of the tile SK_HDR_PREFETCH tiles ahead, so the
+// producer's dependent header loads for it hit L2; 0 = off.  Measured on B200 (same
+// box, 3 rounds, gpurun_out/ab_hdrpf.log): C1 1000^2 w = 1 22.5 -> 20.5 us, 256^3 w = 1
+// 260 -> 250 us, w = 4 374 -> 367 us, w >= 8 unchanged.  The row-contiguous kernels
+// with an epilogue (AXPBY w = 8: 0.70 -> 0.715 ms, also with a runtime flag gate) got a
+// worse schedule, so there it is compiled into the epilogue-free (PLAIN) kernels only.
+#ifndef SK_HDR_PREFETCH
+#define SK_HDR_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_headers(const gidx* chunk_offset, const lidx* chunk_len, gidx c0, int nc,
+                                                 int lane) {
+    // 16 offsets / 32 lengths per 128-B line
+    if (lane * 16 <= nc) prefetch_l2(chunk_offset + c0 + lane * 16);
+    if (lane * 32 < nc) prefetch_l2(chunk_len + c0 + lane * 32);
+}
+
 template <class T, int C, int W, int U>
 __global__ void __launch_bounds__(kBlock) spmv_cw_kernel(const KArgs<T> a) {
     using O = Ops<T>;
@@ -498,6 +515,14 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
                     bulk_g2s(scol, a.col + off0, cb, &full[s], pol);
                 } else {
                     mbar_arrive(&full[s]);
+                }
+            }
+            if constexpr (SK_HDR_PREFETCH > 0) {
+                const gidx tn = tile_of(it + SK_HDR_PREFETCH, seg);
+                if (tn < ntiles) {
+                    const gidx cn0 = a.rg0 * (32 / C) + tn * chunks_per_tile;
+                    const gidx cn1 = min(min(a.nchunks, a.rg1 * (32 / C)), cn0 + chunks_per_tile);
+                    prefetch_headers(a.chunk_offset, a.chunk_len, cn0, int(cn1 - cn0), lane);
                 }
             }
         }
@@ -896,6 +921,14 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                     bulk_g2s(scol, a.col + off0, cb, &full[s], pol);
                 } else {
                     mbar_arrive(&full[s]);
+                }
+            }
+            if constexpr (SK_HDR_PREFETCH > 0 && PLAIN) {
+                const gidx tn = tile_of(it + SK_HDR_PREFETCH, seg);
+                if (tn < ntiles) {
+                    const gidx cn0 = tile_rg(tn) * (32 / C);
+                    const gidx cn1 = min(min(a.nchunks, a.rg1 * (32 / C)), cn0 + chunks_per_tile);
+                    prefetch_headers(a.chunk_offset, a.chunk_len, cn0, int(cn1 - cn0), lane);
                 }
             }
         }
