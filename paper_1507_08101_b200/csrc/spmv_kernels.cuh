@@ -122,7 +122,9 @@ __device__ __forceinline__ bool deferred(const std::uint32_t* mask, gidx row) {
 // box, 3 rounds, gpurun_out/ab_hdrpf.log): C1 1000^2 w = 1 22.5 -> 20.5 us, 256^3 w = 1
 // 260 -> 250 us, w = 4 374 -> 367 us, w >= 8 unchanged.  The row-contiguous kernels
 // with an epilogue (AXPBY w = 8: 0.70 -> 0.715 ms, also with a runtime flag gate) got a
-// worse schedule, so there it is compiled into the epilogue-free (PLAIN) kernels only.
+// worse schedule, so there it is compiled into the epilogue-free (PLAIN) and the dots
+// kernels only (dots, gpurun_out/ab_hdrpf_dots.log: C3 C64 5.85 -> 5.71-5.81 ms row order,
+// 5.03 -> 4.96 ms pencil order, 400^3 w = 1 with three dots 1.047 -> 1.016 ms).
 #ifndef SK_HDR_PREFETCH
 #define SK_HDR_PREFETCH 1
 #endif
@@ -923,7 +925,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                     mbar_arrive(&full[s]);
                 }
             }
-            if constexpr (SK_HDR_PREFETCH > 0 && PLAIN) {
+            if constexpr (SK_HDR_PREFETCH > 0 && (PLAIN || DOTS)) {
                 const gidx tn = tile_of(it + SK_HDR_PREFETCH, seg);
                 if (tn < ntiles) {
                     const gidx cn0 = tile_rg(tn) * (32 / C);
