@@ -22,6 +22,8 @@ extern "C" {
  * semantics).  sync = 0: calls that do not return data to the host only
  * enqueue work on the library stream of their device; sellkit_ext_synchronize
  * waits for it.  The stream is a cudaStream_t (non-blocking). */
+/* Message of the last call on this thread that returned an error ("" if none). */
+const char* sellkit_ext_last_error(void);
 sellkit_error sellkit_ext_set_sync(int sync);
 sellkit_error sellkit_ext_synchronize(void);
 sellkit_error sellkit_ext_stream(void** stream);
@@ -105,6 +107,22 @@ sellkit_error sellkit_ext_rankctx_set_sends(sellkit_rankctx* rc, int to, const s
 sellkit_error sellkit_ext_rankctx_send(const sellkit_rankctx* rc, int s, int* to, sellkit_lidx* count,
                                        sellkit_lidx* local_rows);
 sellkit_error sellkit_ext_rankctx_connect(sellkit_rankctx* rc, const void* id128);
+/* CUDA-IPC transport (all ranks on one node; replaces step 3 above).  Each rank
+ * exports its send slots (sized for blocks of up to max_width columns), its dot slot
+ * and its flag block; blob == NULL queries *blob_bytes.  The caller all-gathers the
+ * blobs (any transport) and passes all nranks of them, in rank order, to
+ * sellkit_ext_rankctx_ipc_connect.  Halo slots are pulled by the receiver with
+ * copy-engine peer copies; ranks signal each other with stream memory operations
+ * (no kernel waits on another rank). */
+sellkit_error sellkit_ext_rankctx_ipc_export(sellkit_rankctx* rc, int max_width, void* blob, size_t* blob_bytes);
+sellkit_error sellkit_ext_rankctx_ipc_connect(sellkit_rankctx* rc, const void* blobs, size_t blob_bytes);
+/* 0 = not connected (world size 1), 1 = NCCL, 2 = IPC */
+sellkit_error sellkit_ext_rankctx_transport(const sellkit_rankctx* rc, int* transport);
+/* graphs: 1 = capture each repeated step (same vectors, flags and scalars) in a CUDA
+ * graph on its second use and replay it (default; SELLKIT_GRAPHS=0 disables),
+ * 0 = always enqueue eagerly; reserve_sms: SMs the local sweep leaves free for the
+ * concurrent halo pack (default SELLKIT_COMM_RESERVE_SMS or 0).  -1 keeps a setting. */
+sellkit_error sellkit_ext_rankctx_set_options(sellkit_rankctx* rc, int graphs, int reserve_sms);
 sellkit_error sellkit_ext_rank_spmv(sellkit_densemat* y, sellkit_rankctx* rc, const sellkit_densemat* x,
                                     const sellkit_spmv_opts* opts, sellkit_densemat* z, int nocomm);
 sellkit_error sellkit_ext_rankctx_stats(const sellkit_rankctx* rc, uint64_t* bytes, uint64_t* msgs,

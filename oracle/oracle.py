@@ -408,3 +408,64 @@ def build_context(rowptr, col, val, k, C_, sigma, orc: Oracle, weights=None, by_
             ranks[owner]["send_to"].append(r)
             ranks[owner]["send_rows"].append(perm[gcols - row_offset[owner]].astype(np.int32))
     return row_offset, ranks
+
+
+# ------------------------------------------------------------ full size --
+
+FULLSIZE_PATH = os.path.join(HERE, "libfullsize.so")
+
+
+class FullSize:
+    """ctypes binding of oracle/libfullsize.so (fullsize.c): OpenMP generators and
+    checkers for the BASELINE-size parity tests and the reference arm's input."""
+
+    def __init__(self, path: str = FULLSIZE_PATH):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -f oracle/Makefile`")
+        L = self.lib = C.CDLL(path)
+        L.fs_hash_block.argtypes = [i64, i32, C.c_uint64, vp]
+        L.fs_stencil7_crs.argtypes = [i64, i64, i64, vp, vp, vp]
+        L.fs_tsmm_rows.argtypes = [i64, i64, i32, i32, C.c_uint64, vp, C.c_double, C.c_double, C.c_uint64, vp]
+        L.fs_tsmttsm.argtypes = [i64, i32, i32, C.c_uint64, C.c_uint64, vp, vp]
+        L.fs_dot_cols.argtypes = [i64, i32, vp, vp, vp, vp]
+        L.fs_zdot_cols.argtypes = [i64, i32, vp, vp, vp, vp]
+
+    def hash_block(self, nrows: int, ncols: int, seed: int) -> np.ndarray:
+        out = np.empty((nrows, ncols), np.float64)
+        self.lib.fs_hash_block(nrows, ncols, seed, _p(out))
+        return out
+
+    def stencil7_crs(self, n: int, r0: int = 0, r1: Optional[int] = None):
+        r1 = n ** 3 if r1 is None else r1
+        rows = r1 - r0
+        rowptr = np.empty(rows + 1, np.int64)
+        nnz_max = 7 * rows
+        col = np.empty(nnz_max, np.int64)
+        val = np.empty(nnz_max, np.float64)
+        self.lib.fs_stencil7_crs(n, r0, r1, _p(rowptr), _p(col), _p(val))
+        nnz = int(rowptr[-1])
+        return rowptr, col[:nnz], val[:nnz]
+
+    def tsmm_rows(self, i0: int, i1: int, m: int, k: int, seed_v: int, x: np.ndarray, alpha: float, beta: float,
+                  seed_w: int) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.empty((i1 - i0, k), np.float64)
+        self.lib.fs_tsmm_rows(i0, i1, m, k, seed_v, _p(x), alpha, beta, seed_w, _p(out))
+        return out
+
+    def tsmttsm(self, n: int, m: int, k: int, seed_v: int, seed_w: int):
+        x, sc = np.empty((m, k), np.float64), np.empty((m, k), np.float64)
+        self.lib.fs_tsmttsm(n, m, k, seed_v, seed_w, _p(x), _p(sc))
+        return x, sc
+
+    def dot_cols(self, a: np.ndarray, b: np.ndarray):
+        """long-double column dots of two row-major blocks: (dots, sum |a b|) per column."""
+        if np.iscomplexobj(a):
+            a, b = np.ascontiguousarray(a, np.complex128), np.ascontiguousarray(b, np.complex128)
+            out, sc = np.empty(a.shape[1], np.complex128), np.empty(a.shape[1], np.float64)
+            self.lib.fs_zdot_cols(a.shape[0], a.shape[1], _p(a), _p(b), _p(out), _p(sc))
+            return out, sc
+        a, b = np.ascontiguousarray(a, np.float64), np.ascontiguousarray(b, np.float64)
+        out, sc = np.empty(a.shape[1], np.float64), np.empty(a.shape[1], np.float64)
+        self.lib.fs_dot_cols(a.shape[0], a.shape[1], _p(a), _p(b), _p(out), _p(sc))
+        return out, sc

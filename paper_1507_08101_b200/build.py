@@ -1,13 +1,13 @@
-"""Build the B200 library (and, for tests/bench only, the CPU oracle).
+"""Build the B200 library in-tree (paper_1507_08101_b200/lib/libsellkit_b200.so).
 
-    python -m paper_1507_08101_b200.build            # product library only
-    python -m paper_1507_08101_b200.build --all      # + oracle/liboracle.so + oracle/_ref (if /root/reference exists)
+    python -m paper_1507_08101_b200.build
+
+The CPU checkers are test infrastructure and build separately (python -m oracle.build).
 """
 from __future__ import annotations
 
 import os
 import subprocess
-import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -27,14 +27,5 @@ def build_library(jobs: int = 0) -> str:
     return LIB
 
 
-def build_oracle() -> None:
-    """The CPU checker (test infrastructure, never linked by the product)."""
-    _run(["make", "-f", "oracle/Makefile"])
-    if os.path.isdir("/root/reference/proj"):
-        _run(["make", f"-j{max(1, os.cpu_count() or 1)}", "-f", "oracle/Makefile.ref"])
-
-
 if __name__ == "__main__":
     build_library()
-    if "--all" in sys.argv:
-        build_oracle()

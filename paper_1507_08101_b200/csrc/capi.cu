@@ -614,6 +614,8 @@ void sellkit_region_destroy(sellkit_region* region) { delete region; }
 
 /* ------------------------------------------------------------ extensions -- */
 
+const char* sellkit_ext_last_error(void) { return sk::last_error_message(); }
+
 sellkit_error sellkit_ext_set_sync(int sync) {
     return guarded([&] { sk::set_sync_mode(sync != 0); });
 }

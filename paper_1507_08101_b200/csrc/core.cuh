@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstring>
@@ -190,6 +191,8 @@ struct DeviceRuntime {
 
 DeviceRuntime& runtime(int device);
 int current_device();
+void set_last_error(const char* msg);  // per-thread message of the last failed C-ABI call
+const char* last_error_message();
 bool sync_mode();          // true: public calls synchronise before returning
 void set_sync_mode(bool);
 
@@ -204,6 +207,15 @@ struct DeviceGuard {
 };
 
 void finish(DeviceRuntime& rt);  // sync if sync_mode(), else check launch errors
+
+// NVTX range (host side) around a library phase: visible in Nsight timelines, a no-op
+// without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Where does a caller pointer live?
 enum class MemKind { device, host };

@@ -1,5 +1,6 @@
 // Row-distributed SpMMV with halo exchange.  Design: dist.cuh.
 // Reference: /root/reference/proj/src/partition.hpp.
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -290,16 +291,22 @@ void rank_build_device(RankPart& part, lidx C, lidx sigma) {
 
 namespace {
 
-std::vector<lidx> download_perm(const SellMat& m) {
+std::vector<lidx> download_perm_uncached(const SellMat& m) {
     std::vector<lidx> h(std::size_t(m.nrows));
     DeviceGuard g(m.device);
     CK(cudaMemcpy(h.data(), m.row_perm.get(), h.size() * sizeof(lidx), cudaMemcpyDeviceToHost));
     return h;
 }
 
+// original local row -> stored row of a rank's local part, downloaded once
+const std::vector<lidx>& rank_perm(const RankPart& part) {
+    if (part.perm_host.size() != std::size_t(part.plan.nrows)) part.perm_host = download_perm_uncached(*part.local);
+    return part.perm_host;
+}
+
 // send rows in the owner's stored space (partition.hpp:274-275)
 void build_send_rows(RankPart& part) {
-    const std::vector<lidx> perm = download_perm(*part.local);
+    const std::vector<lidx>& perm = rank_perm(part);
     DeviceGuard g(part.device);
     auto& rt = runtime(part.device);
     part.send_rows.clear();
@@ -327,8 +334,11 @@ void ensure_scratch(RankScratch& s, const RankPart& part, lidx w) {
 }
 
 // local sweep (+ deferred-row hooks) and remote sweep of one rank; dots -> scratch.dots
+// `extra` supplies the sweeps' scratch (graph-stable, rank-owned) and the SMs the
+// local sweep leaves to a concurrent halo pack; stream/dot fields are set here.
 void rank_sweeps(RankPart& part, RankScratch& sc, DenseMat& y, const DenseMat& x, const SpmvOptions& o, DenseMat* z,
-                 bool nocomm, cudaStream_t st, const std::function<void()>& before_remote) {
+                 bool nocomm, cudaStream_t st, const std::function<void()>& before_remote,
+                 const SpmvHooks& extra = SpmvHooks{}) {
     const std::uint32_t dots = o.flags & kFlagDots;
     const bool chain = (o.flags & kFlagChain) != 0;
     const bool has_remote = part.remote != nullptr && !nocomm;
@@ -336,6 +346,9 @@ void rank_sweeps(RankPart& part, RankScratch& sc, DenseMat& y, const DenseMat& x
     base.dot = nullptr;
     base.z = chain ? z : nullptr;
     SpmvHooks hl;
+    hl.scratch = extra.scratch;
+    hl.scratch_size = extra.scratch_size;
+    hl.reserve_sms = extra.reserve_sms;
     hl.stream = st;
     hl.accumulate_dots = true;
     hl.dot_accum = sc.dots.get();
@@ -359,6 +372,8 @@ void rank_sweeps(RankPart& part, RankScratch& sc, DenseMat& y, const DenseMat& x
     DenseMat halo = densemat_view_plain(part.plan.dt, sc.halo.get(), part.plan.halo_cols.size() * x.ncols,
                                         lidx(part.plan.halo_cols.size()), x.ncols, x.ncols, Order::row_major);
     SpmvHooks hr;
+    hr.scratch = extra.scratch;
+    hr.scratch_size = extra.scratch_size;
     hr.stream = st;
     hr.row_map = part.row_map.as<lidx>();
     hr.accumulate_dots = true;
@@ -415,18 +430,25 @@ std::unique_ptr<DistContext> dist_context_create(const Crs& a, const std::vector
         rank_build_device(*ctx->ranks[r], C, sigma);
         build_send_rows(*ctx->ranks[r]);
     }
-    // peer access between the devices in use (halo stores go straight into the peer's buffer)
-    for (int i = 0; i < std::min(k, ndev); ++i)
-        for (int j = 0; j < std::min(k, ndev); ++j) {
+    // peer access between the devices the ranks use (halo stores go straight into the
+    // peer's buffer); the pairs that were enabled decide the direct-store path
+    ctx->ndev = ndev;
+    ctx->peer_ok.assign(std::size_t(ndev) * ndev, 0);
+    std::vector<int> used;
+    for (auto& part : ctx->ranks)
+        if (std::find(used.begin(), used.end(), part->device) == used.end()) used.push_back(part->device);
+    for (int i : used)
+        for (int j : used) {
             if (i == j) continue;
             int ok = 0;
-            cudaDeviceCanAccessPeer(&ok, i, j);
+            if (cudaDeviceCanAccessPeer(&ok, i, j) != cudaSuccess) ok = 0;
             if (ok) {
                 DeviceGuard g(i);
-                cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
-                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+                ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
                 cudaGetLastError();
             }
+            ctx->peer_ok[std::size_t(i) * ndev + j] = char(ok);
         }
     ctx->scratch.resize(std::size_t(k));
     return ctx;
@@ -453,7 +475,7 @@ void dist_scatter(const DistContext& ctx, const DenseMat& global, DistVec& v) {
     densemat_copy_out(global, host.data(), std::size_t(ctx.n) * w);
     for (std::size_t r = 0; r < ctx.ranks.size(); ++r) {
         const auto& part = *ctx.ranks[r];
-        const std::vector<lidx> perm = download_perm(*part.local);
+        const std::vector<lidx>& perm = rank_perm(part);
         std::vector<unsigned char> buf(std::size_t(part.plan.nrows) * w * es);
         for (lidx i = 0; i < part.plan.nrows; ++i)
             std::memcpy(&buf[std::size_t(perm[i]) * w * es], &host[std::size_t(part.plan.first_row + i) * w * es],
@@ -471,7 +493,7 @@ void dist_gather(const DistContext& ctx, const DistVec& v, DenseMat& out) {
     std::vector<unsigned char> host(std::size_t(ctx.n) * w * es);
     for (std::size_t r = 0; r < ctx.ranks.size(); ++r) {
         const auto& part = *ctx.ranks[r];
-        const std::vector<lidx> perm = download_perm(*part.local);
+        const std::vector<lidx>& perm = rank_perm(part);
         std::vector<unsigned char> buf(std::size_t(part.plan.nrows) * w * es);
         {
             DeviceGuard g(part.device);
@@ -520,8 +542,7 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
                 const lidx cnt = lidx(part.plan.send_local_rows[s].size());
                 auto* dptr = static_cast<unsigned char*>(ctx.scratch[to].halo.get()) +
                              std::size_t(dp.recv_offset[q]) * w * es;
-                int can = dst.device == part.device;
-                if (!can) cudaDeviceCanAccessPeer(&can, part.device, dst.device);
+                const bool can = ctx.direct(part.device, dst.device);
                 const DenseMat& xr = x.parts[r];
                 visit_dt(ctx.dt, [&]<class T>() {
                     T* out = can ? reinterpret_cast<T*>(dptr) : ctx.scratch[r].sendbuf.as<T>();
@@ -558,40 +579,32 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
                     });
         CK(cudaEventRecord(part.ev_done, rt.stream));
     }
-    // 3. dots: per-rank partials summed in rank order (partition.hpp:379-394)
+    // 3. dots: per-rank partials summed in rank order on rank 0's device
+    //    (partition.hpp:379-394), one copy of the requested thirds to the caller
     if (dots) {
-        std::vector<unsigned char> all(std::size_t(k) * 3 * w * es);
+        RankPart& p0 = *ctx.ranks[0];
+        DeviceGuard g(p0.device);
+        auto& rt0 = runtime(p0.device);
+        const std::size_t db = 3 * std::size_t(w) * es;
+        if (ctx.dots_all.bytes() < std::size_t(k) * db) ctx.dots_all = DeviceBuffer(std::size_t(k) * db, p0.device);
+        auto* all = static_cast<unsigned char*>(ctx.dots_all.get());
         for (int r = 0; r < k; ++r) {
-            DeviceGuard g(ctx.ranks[r]->device);
-            auto& rt = runtime(ctx.ranks[r]->device);
-            CK(cudaMemcpyAsync(&all[std::size_t(r) * 3 * w * es], ctx.scratch[r].dots.get(), 3 * w * es,
-                               cudaMemcpyDeviceToHost, rt.stream));
-            CK(cudaStreamSynchronize(rt.stream));
+            RankPart& part = *ctx.ranks[r];
+            if (r > 0) CK(cudaStreamWaitEvent(rt0.stream, part.ev_done, 0));
+            CK(cudaMemcpyPeerAsync(all + std::size_t(r) * db, p0.device, ctx.scratch[r].dots.get(), part.device, db,
+                                   rt0.stream));
         }
-        std::vector<unsigned char> res(3 * w * es);
         visit_dt(ctx.dt, [&]<class T>() {
-            T* out = reinterpret_cast<T*>(res.data());
-            const T* in = reinterpret_cast<const T*>(all.data());
-            for (int t = 0; t < 3 * w; ++t) {
-                T s = in[t];
-                for (int r = 1; r < k; ++r) {
-                    if constexpr (scalar_traits<T>::is_complex) {
-                        s.re += in[std::size_t(r) * 3 * w + t].re;
-                        s.im += in[std::size_t(r) * 3 * w + t].im;
-                    } else {
-                        s += in[std::size_t(r) * 3 * w + t];
-                    }
-                }
-                out[t] = s;
-            }
+            rank_sum_kernel<T><<<(3 * w + 127) / 128, 128, 0, rt0.stream>>>(ctx.dots_all.as<T>(), k, 3 * w,
+                                                                           ctx.scratch[0].dots.as<T>());
             return 0;
         });
+        CK(cudaGetLastError());
         for (int s = 0; s < 3; ++s)
-            if (o.flags & (kFlagDotYY << s)) {
-                DeviceGuard g(ctx.ranks[0]->device);
-                CK(cudaMemcpy(static_cast<unsigned char*>(o.dot) + std::size_t(s) * w * es, &res[std::size_t(s) * w * es],
-                              w * es, cudaMemcpyDefault));
-            }
+            if (o.flags & (kFlagDotYY << s))
+                CK(cudaMemcpyAsync(static_cast<unsigned char*>(o.dot) + std::size_t(s) * w * es,
+                                   static_cast<unsigned char*>(ctx.scratch[0].dots.get()) + std::size_t(s) * w * es,
+                                   w * es, cudaMemcpyDefault, rt0.stream));
         if (ctx.record && k > 1) {
             ctx.msgs += 2 * std::uint64_t(k - 1);
             ctx.bytes += 2 * std::uint64_t(k - 1) * 3 * w * es;
@@ -605,16 +618,195 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
 }
 
 // ------------------------------------------------------ one process per GPU
+//
+// Transports of the per-process rank context:
+//   nccl : pack -> ncclSend/ncclRecv pairs in one group on the comm stream; dots
+//          all-gathered with NCCL and summed in rank order.
+//   ipc  : every rank exports (CUDA IPC) a send buffer with one slot per
+//          destination, a dot-partial slot and a flag block.  The owner packs its
+//          send lists into its own slots (a local gather kernel), then raises the
+//          receiver's "full" flag; the receiver pulls its slot with a copy-engine
+//          peer copy (NVLink on a multi-GPU node, no SMs taken from the local sweep)
+//          and raises the owner's "free" flag.  Flags are 0/1 handshakes written and
+//          waited on by stream memory operations (cuStreamWriteValue32 /
+//          cuStreamWaitValue32): no kernel ever waits on another rank, and the
+//          values are the same every step, so the whole step can be captured in a
+//          CUDA graph.  Dots travel the same way (a 3w slot per rank).
+
+namespace {
+
+// driver entry points resolved through the runtime (no link-time libcuda dependency)
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <class F>
+F driver_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPointByVersion(name, &fn, 12000, cudaEnableDefault, &q));
+    SK_REQUIRE(fn != nullptr && q == cudaDriverEntryPointSuccess, errc::unsupported,
+               std::string("driver entry point unavailable: ") + name);
+    return reinterpret_cast<F>(fn);
+}
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS)
+        fail(errc::transport, std::string("CUDA driver error ") + std::to_string(int(r)) + " in " + what);
+}
+
+void flag_wait(cudaStream_t st, const std::uint32_t* addr, std::uint32_t v) {
+    static const WaitValueFn fn = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+    cu_check(fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_EQ),
+             "cuStreamWaitValue32");
+}
+
+void flag_set(cudaStream_t st, std::uint32_t* addr, std::uint32_t v) {
+    // default flags: the write is ordered after (and fenced against) the stream's earlier work
+    static const WriteValueFn fn = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+    cu_check(fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WRITE_VALUE_DEFAULT),
+             "cuStreamWriteValue32");
+}
+
+constexpr char kIpcMagic[8] = {'S', 'K', 'I', 'P', 'C', '0', '1', 0};
+
+struct IpcBlobHead {
+    char magic[8];
+    int rank, nranks, max_w, es, device, pad;
+    cudaIpcMemHandle_t send, dots, flags;
+};
+// followed by gidx seg_row[nranks]: first row of destination d's slot in the send buffer (-1: none)
+
+std::size_t ipc_blob_bytes(int nranks) { return sizeof(IpcBlobHead) + std::size_t(nranks) * sizeof(gidx); }
+
+// 16-byte units of whole rows (row bytes and strides multiples of 16)
+__global__ void pack16_kernel(const int4* x, gidx x_rs16, const lidx* rows, lidx count, int u, int4* out) {
+    const gidx total = gidx(count) * u;
+    for (gidx t = blockIdx.x * gidx(blockDim.x) + threadIdx.x; t < total; t += gidx(gridDim.x) * blockDim.x) {
+        const gidx i = t / u;
+        const int j = int(t - i * u);
+        out[t] = x[gidx(__ldg(rows + i)) * x_rs16 + j];
+    }
+}
+
+// gather x rows `rows[0..cnt)` (all `w` columns) into out[cnt x w]
+void launch_pack(Datatype dt, const DenseMat& x, const lidx* rows, lidx cnt, lidx w, void* out, cudaStream_t st) {
+    if (cnt == 0) return;
+    const std::size_t es = value_bytes(dt);
+    const std::size_t rb = std::size_t(w) * es;
+    const bool vec = x.order == Order::row_major && rb % 16 == 0 &&
+                     (std::size_t(x.row_stride()) * es) % 16 == 0 && reinterpret_cast<std::uintptr_t>(x.data) % 16 == 0 &&
+                     reinterpret_cast<std::uintptr_t>(out) % 16 == 0;
+    if (vec) {
+        const int u = int(rb / 16);
+        pack16_kernel<<<pack_grid(gidx(cnt) * u), 256, 0, st>>>(reinterpret_cast<const int4*>(x.data),
+                                                                 gidx(std::size_t(x.row_stride()) * es / 16), rows,
+                                                                 cnt, u, static_cast<int4*>(out));
+    } else {
+        visit_dt(dt, [&]<class T>() {
+            pack_kernel<T><<<pack_grid(gidx(cnt) * w), 256, 0, st>>>(
+                reinterpret_cast<const T*>(x.data), x.row_stride(), x.col_step(), rows, cnt, w, static_cast<T*>(out));
+            return 0;
+        });
+    }
+    CK(cudaGetLastError());
+}
+
+// identity of one step: everything a captured graph bakes in
+struct StepKey {
+    const void* y = nullptr;
+    const void* x = nullptr;
+    const void* z = nullptr;
+    const void* gl = nullptr;
+    const void* dot = nullptr;
+    std::uint32_t flags = 0;
+    lidx w = 0;
+    int nocomm = 0;
+    unsigned char sc[5][16] = {};
+    bool operator==(const StepKey& o) const { return std::memcmp(this, &o, sizeof(StepKey)) == 0; }
+};
+
+StepKey make_key(const DenseMat& y, const DenseMat& x, const SpmvOptions& o, const DenseMat* z, bool nocomm) {
+    StepKey k;
+    std::memset(&k, 0, sizeof(k));  // padding bytes take part in the comparison
+    k.y = y.data;
+    k.x = x.data;
+    k.z = z ? z->data : nullptr;
+    k.gl = o.gamma_list;
+    k.dot = o.dot;
+    k.flags = o.flags;
+    k.w = x.ncols;
+    k.nocomm = nocomm ? 1 : 0;
+    std::memcpy(k.sc[0], o.alpha, 16);
+    std::memcpy(k.sc[1], o.beta, 16);
+    std::memcpy(k.sc[2], o.gamma, 16);
+    std::memcpy(k.sc[3], o.delta, 16);
+    std::memcpy(k.sc[4], o.eta, 16);
+    return k;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+}  // namespace
 
 struct RankContext {
     RankPart part;
     RankScratch sc;
+    Transport transport = Transport::none;
     ncclComm_t comm = nullptr;
     lidx C = 1, sigma = 1;
     bool sends_ready = false;
     std::uint64_t bytes = 0, msgs = 0;
-    DeviceBuffer dots_all;
+    DeviceBuffer dots_all;       // nranks x 3w partials
+    DeviceBuffer sweep_scratch;  // the sweeps' scratch (graph-stable)
+    lidx buf_width = 0;
+    // ipc transport
+    int ipc_max_w = 0;
+    DeviceBuffer ipc_send, ipc_dots, ipc_flags;
+    std::vector<gidx> seg_row;  // per destination rank: first row of its slot (-1: none)
+    struct Peer {
+        unsigned char* send = nullptr;
+        unsigned char* dots = nullptr;
+        std::uint32_t* flags = nullptr;
+        gidx seg_for_me = -1;
+    };
+    std::vector<Peer> peers;
+    // CUDA graphs of whole steps, keyed by StepKey (captured on the second use)
+    struct Graph {
+        StepKey key;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<Graph> graphs;
+    bool graphs_on = env_int("SELLKIT_GRAPHS", 1) != 0;
+    bool graphs_broken = false;
+    int reserve_sms = env_int("SELLKIT_COMM_RESERVE_SMS", 0);
+    cudaStream_t cap = nullptr;
+    cudaEvent_t cev_x = nullptr, cev_halo = nullptr;  // fork/join events of captured steps
+    ~RankContext();
+    void drop_graphs() {
+        for (auto& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
 };
+
+RankContext::~RankContext() {
+    DeviceGuard g(part.device);
+    cudaDeviceSynchronize();
+    drop_graphs();
+    for (auto& p : peers) {
+        if (p.send) cudaIpcCloseMemHandle(p.send);
+        if (p.dots) cudaIpcCloseMemHandle(p.dots);
+        if (p.flags) cudaIpcCloseMemHandle(p.flags);
+    }
+    if (comm) ncclCommDestroy(comm);
+    if (cap) cudaStreamDestroy(cap);
+    if (cev_x) cudaEventDestroy(cev_x);
+    if (cev_halo) cudaEventDestroy(cev_halo);
+    cudaGetLastError();
+}
 
 RankContext* rankctx_create(const Crs& rows, const std::vector<gidx>& row_offset, int rank, lidx C, lidx sigma) {
     SK_REQUIRE(row_offset.size() >= 2, errc::invalid_arg, "partition needs at least one rank");
@@ -653,90 +845,395 @@ void nccl_unique_id(void* out128) {
 }
 
 void rankctx_connect(RankContext* rc, const void* nccl_id) {
+    SK_REQUIRE(rc->transport == Transport::none, errc::state, "rank context is already connected");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     DeviceGuard g(rc->part.device);
     NCK(ncclCommInitRank(&rc->comm, rc->part.plan.nranks, id, rc->part.plan.rank));
+    rc->transport = Transport::nccl;
 }
+
+std::size_t rankctx_ipc_blob_bytes(RankContext* rc) { return ipc_blob_bytes(rc->part.plan.nranks); }
+
+// allocate and export this rank's IPC buffers (send slots sized for max_w columns)
+void rankctx_ipc_export(RankContext* rc, int max_w, void* blob) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    SK_REQUIRE(rc->transport == Transport::none, errc::state, "rank context is already connected");
+    SK_REQUIRE(max_w >= 1, errc::invalid_arg, "max_width must be positive");
+    DeviceGuard g(part.device);
+    const std::size_t es = value_bytes(p.dt);
+    const int n = p.nranks;
+    if (!rc->ipc_flags.get() || rc->ipc_max_w != max_w) {
+        rc->seg_row.assign(std::size_t(n), -1);
+        gidx rows = 0;
+        for (std::size_t s = 0; s < p.send_to.size(); ++s) {
+            rc->seg_row[p.send_to[s]] = rows;
+            rows += gidx(p.send_local_rows[s].size());
+        }
+        rc->ipc_max_w = max_w;
+        rc->ipc_send = DeviceBuffer(std::max<std::size_t>(std::size_t(rows) * max_w * es, 256), part.device);
+        rc->ipc_dots = DeviceBuffer(std::max<std::size_t>(3 * std::size_t(max_w) * es, 256), part.device);
+        rc->ipc_flags = DeviceBuffer(4 * std::size_t(n) * sizeof(std::uint32_t), part.device);
+        // full = 0, free = 1, dots full = 0, dots free = 1
+        std::vector<std::uint32_t> init(4 * std::size_t(n), 0u);
+        for (int d = 0; d < n; ++d) init[n + d] = init[3 * n + d] = 1u;
+        CK(cudaMemcpy(rc->ipc_flags.get(), init.data(), init.size() * sizeof(std::uint32_t), cudaMemcpyHostToDevice));
+    }
+    IpcBlobHead h;
+    std::memset(&h, 0, sizeof(h));
+    std::memcpy(h.magic, kIpcMagic, sizeof(kIpcMagic));
+    h.rank = p.rank;
+    h.nranks = n;
+    h.max_w = max_w;
+    h.es = int(es);
+    h.device = part.device;
+    CK(cudaIpcGetMemHandle(&h.send, rc->ipc_send.get()));
+    CK(cudaIpcGetMemHandle(&h.dots, rc->ipc_dots.get()));
+    CK(cudaIpcGetMemHandle(&h.flags, rc->ipc_flags.get()));
+    std::memcpy(blob, &h, sizeof(h));
+    std::memcpy(static_cast<unsigned char*>(blob) + sizeof(h), rc->seg_row.data(), std::size_t(n) * sizeof(gidx));
+}
+
+// open every peer's buffers (blobs of all ranks, in rank order)
+void rankctx_ipc_connect(RankContext* rc, const void* blobs, std::size_t blob_bytes) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const int n = p.nranks;
+    SK_REQUIRE(rc->transport == Transport::none, errc::state, "rank context is already connected");
+    SK_REQUIRE(rc->ipc_flags.get() != nullptr, errc::state, "export the IPC buffers first");
+    SK_REQUIRE(blob_bytes == ipc_blob_bytes(n), errc::invalid_arg, "IPC blob size mismatch");
+    DeviceGuard g(part.device);
+    rc->peers.assign(std::size_t(n), RankContext::Peer{});
+    const auto* b = static_cast<const unsigned char*>(blobs);
+    for (int r = 0; r < n; ++r) {
+        IpcBlobHead h;
+        std::memcpy(&h, b + std::size_t(r) * blob_bytes, sizeof(h));
+        SK_REQUIRE(std::memcmp(h.magic, kIpcMagic, sizeof(kIpcMagic)) == 0 && h.rank == r && h.nranks == n,
+                   errc::transport, "malformed IPC blob");
+        SK_REQUIRE(h.max_w == rc->ipc_max_w && h.es == int(value_bytes(p.dt)), errc::transport,
+                   "ranks disagree on the IPC slot geometry");
+        if (r == p.rank) continue;
+        std::vector<gidx> seg(static_cast<std::size_t>(n));
+        std::memcpy(seg.data(), b + std::size_t(r) * blob_bytes + sizeof(h), std::size_t(n) * sizeof(gidx));
+        auto& peer = rc->peers[r];
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, h.send, cudaIpcMemLazyEnablePeerAccess));
+        peer.send = static_cast<unsigned char*>(ptr);
+        CK(cudaIpcOpenMemHandle(&ptr, h.dots, cudaIpcMemLazyEnablePeerAccess));
+        peer.dots = static_cast<unsigned char*>(ptr);
+        CK(cudaIpcOpenMemHandle(&ptr, h.flags, cudaIpcMemLazyEnablePeerAccess));
+        peer.flags = static_cast<std::uint32_t*>(ptr);
+        peer.seg_for_me = seg[p.rank];
+    }
+    for (int owner : p.recv_owner)
+        SK_REQUIRE(rc->peers[owner].seg_for_me >= 0, errc::transport, "an owner has no send slot for this rank");
+    rc->transport = Transport::ipc;
+}
+
+namespace {
+
+// width-dependent buffers; reallocation invalidates every captured graph
+void ensure_rank_buffers(RankContext* rc, lidx w) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const std::size_t es = value_bytes(p.dt);
+    ensure_scratch(rc->sc, part, w);
+    if (rc->buf_width == w) return;
+    auto& rt = runtime(part.device);
+    CK(cudaDeviceSynchronize());
+    rc->drop_graphs();
+    rc->dots_all = DeviceBuffer(std::max<std::size_t>(std::size_t(p.nranks) * 3 * w * es, 256), part.device);
+    const std::size_t ss = spmv_scratch_bytes(p.dt, w, rt.num_sms);
+    rc->sweep_scratch = DeviceBuffer(ss, part.device);
+    rc->buf_width = w;
+}
+
+void ipc_exchange(RankContext* rc, const DenseMat& x, lidx w) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const int n = p.nranks, me = p.rank;
+    const std::size_t es = value_bytes(p.dt);
+    const std::size_t slot_row = std::size_t(rc->ipc_max_w) * es;  // slot pitch per row
+    std::uint32_t* flags = rc->ipc_flags.as<std::uint32_t>();
+    cudaStream_t cs = part.comm;
+    auto* mine = static_cast<unsigned char*>(rc->ipc_send.get());
+    // 1. my slots are free once each receiver pulled the previous step's data
+    for (int d : p.send_to) {
+        flag_wait(cs, flags + n + d, 1u);
+        flag_set(cs, flags + n + d, 0u);
+    }
+    // 2. pack each send list into its slot, 3. raise the receiver's full flag
+    for (std::size_t s = 0; s < p.send_to.size(); ++s) {
+        const int to = p.send_to[s];
+        const lidx cnt = lidx(p.send_local_rows[s].size());
+        launch_pack(p.dt, x, part.send_rows[s].as<lidx>(), cnt, w, mine + std::size_t(rc->seg_row[to]) * slot_row, cs);
+        rc->bytes += std::uint64_t(cnt) * w * es;
+        rc->msgs += 1;
+    }
+    for (int d : p.send_to) flag_set(cs, rc->peers[d].flags + me, 1u);
+    // 4. pull every owner's slot into the halo block (copy engine), release the slot
+    for (std::size_t q = 0; q < p.recv_owner.size(); ++q) {
+        const int s = p.recv_owner[q];
+        const auto& peer = rc->peers[s];
+        flag_wait(cs, flags + s, 1u);
+        CK(cudaMemcpyAsync(static_cast<unsigned char*>(rc->sc.halo.get()) + std::size_t(p.recv_offset[q]) * w * es,
+                           peer.send + std::size_t(peer.seg_for_me) * slot_row, std::size_t(p.recv_count[q]) * w * es,
+                           cudaMemcpyDeviceToDevice, cs));
+        flag_set(cs, flags + s, 0u);
+        flag_set(cs, peer.flags + n + me, 1u);
+    }
+}
+
+void nccl_exchange(RankContext* rc, const DenseMat& x, lidx w) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const std::size_t es = value_bytes(p.dt);
+    std::size_t mult = 1;
+    const ncclDataType_t nt = nccl_type(p.dt, mult);
+    std::size_t off = 0;
+    std::vector<std::size_t> soff;
+    for (std::size_t s = 0; s < p.send_to.size(); ++s) {
+        const lidx cnt = lidx(p.send_local_rows[s].size());
+        soff.push_back(off);
+        launch_pack(p.dt, x, part.send_rows[s].as<lidx>(), cnt, w,
+                    static_cast<unsigned char*>(rc->sc.sendbuf.get()) + off * es, part.comm);
+        off += std::size_t(cnt) * w;
+    }
+    NCK(ncclGroupStart());
+    for (std::size_t q = 0; q < p.recv_owner.size(); ++q)
+        NCK(ncclRecv(static_cast<unsigned char*>(rc->sc.halo.get()) + std::size_t(p.recv_offset[q]) * w * es,
+                     std::size_t(p.recv_count[q]) * w * mult, nt, p.recv_owner[q], rc->comm, part.comm));
+    for (std::size_t s = 0; s < p.send_to.size(); ++s) {
+        const std::size_t cnt = p.send_local_rows[s].size();
+        NCK(ncclSend(static_cast<unsigned char*>(rc->sc.sendbuf.get()) + soff[s] * es, cnt * w * mult, nt,
+                     p.send_to[s], rc->comm, part.comm));
+        rc->bytes += cnt * w * es;
+        rc->msgs += 1;
+    }
+    NCK(ncclGroupEnd());
+}
+
+// per-rank dot partials (sc.dots) -> every rank's dots_all in rank order -> rank-ordered sum
+void combine_dots(RankContext* rc, lidx w, cudaStream_t st) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const int n = p.nranks, me = p.rank;
+    const std::size_t es = value_bytes(p.dt);
+    const std::size_t db = 3 * std::size_t(w) * es;
+    auto* all = static_cast<unsigned char*>(rc->dots_all.get());
+    if (rc->transport == Transport::nccl) {
+        std::size_t mult = 1;
+        const ncclDataType_t nt = nccl_type(p.dt, mult);
+        NCK(ncclAllGather(rc->sc.dots.get(), all, 3 * std::size_t(w) * mult, nt, rc->comm, st));
+    } else {
+        std::uint32_t* flags = rc->ipc_flags.as<std::uint32_t>();
+        for (int d = 0; d < n; ++d)
+            if (d != me) {
+                flag_wait(st, flags + 3 * n + d, 1u);
+                flag_set(st, flags + 3 * n + d, 0u);
+            }
+        CK(cudaMemcpyAsync(rc->ipc_dots.get(), rc->sc.dots.get(), db, cudaMemcpyDeviceToDevice, st));
+        for (int d = 0; d < n; ++d)
+            if (d != me) flag_set(st, rc->peers[d].flags + 2 * n + me, 1u);
+        for (int s = 0; s < n; ++s) {
+            if (s == me) {
+                CK(cudaMemcpyAsync(all + std::size_t(s) * db, rc->sc.dots.get(), db, cudaMemcpyDeviceToDevice, st));
+                continue;
+            }
+            flag_wait(st, flags + 2 * n + s, 1u);
+            CK(cudaMemcpyAsync(all + std::size_t(s) * db, rc->peers[s].dots, db, cudaMemcpyDeviceToDevice, st));
+            flag_set(st, flags + 2 * n + s, 0u);
+            flag_set(st, rc->peers[s].flags + 3 * n + me, 1u);
+        }
+    }
+    visit_dt(p.dt, [&]<class T>() {
+        rank_sum_kernel<T><<<(3 * w + 127) / 128, 128, 0, st>>>(rc->dots_all.as<T>(), n, 3 * w, rc->sc.dots.as<T>());
+        return 0;
+    });
+    CK(cudaGetLastError());
+    rc->msgs += 2 * std::uint64_t(n - 1);
+    rc->bytes += 2 * std::uint64_t(n - 1) * db;
+}
+
+// enqueue one distributed step on `st` (+ the comm stream); `capturing`: inside a
+// graph capture (consecutive graph launches are ordered by the stream instead of ev_done)
+void rank_step(RankContext* rc, DenseMat& y, const DenseMat& x, const SpmvOptions& o, DenseMat* z, bool nocomm,
+               cudaStream_t st, bool capturing) {
+    RankPart& part = rc->part;
+    const RankPlan& p = part.plan;
+    const lidx w = x.ncols;
+    const std::size_t es = value_bytes(p.dt);
+    const std::uint32_t dots = o.flags & kFlagDots;
+    const bool exchange = !nocomm && p.nranks > 1 && (!p.send_to.empty() || !p.recv_owner.empty());
+    // events recorded inside a capture cannot be waited on outside it: captures use their own
+    cudaEvent_t ev_x = capturing ? rc->cev_x : part.ev_x;
+    cudaEvent_t ev_halo = capturing ? rc->cev_halo : part.ev_halo;
+    if (exchange) {
+        NvtxRange r("sellkit halo exchange (enqueue)");
+        CK(cudaEventRecord(ev_x, st));
+        CK(cudaStreamWaitEvent(part.comm, ev_x, 0));
+        if (!capturing) CK(cudaStreamWaitEvent(part.comm, part.ev_done, 0));  // previous remote sweep used the halo
+        if (rc->transport == Transport::ipc) ipc_exchange(rc, x, w);
+        else nccl_exchange(rc, x, w);
+        CK(cudaEventRecord(ev_halo, part.comm));
+    }
+    SpmvHooks extra;
+    extra.scratch = rc->sweep_scratch.get();
+    extra.scratch_size = rc->sweep_scratch.bytes();
+    extra.reserve_sms = exchange && !p.send_to.empty() ? rc->reserve_sms : 0;
+    {
+        NvtxRange r("sellkit local + remote sweeps (enqueue)");
+        rank_sweeps(part, rc->sc, y, x, o, z, !exchange && (nocomm || p.recv_owner.empty()), st,
+                    [&] { CK(cudaStreamWaitEvent(st, ev_halo, 0)); }, extra);
+    }
+    if (exchange) CK(cudaStreamWaitEvent(st, ev_halo, 0));  // join the comm branch
+    // (graph launches are ordered by the stream; only eager steps publish ev_done)
+    if (!capturing) CK(cudaEventRecord(part.ev_done, st));
+    if (dots) {
+        NvtxRange r("sellkit dots (enqueue)");
+        if (p.nranks > 1 && rc->transport != Transport::none) combine_dots(rc, w, st);
+        for (int s = 0; s < 3; ++s)
+            if (o.flags & (kFlagDotYY << s))
+                CK(cudaMemcpyAsync(static_cast<unsigned char*>(o.dot) + std::size_t(s) * w * es,
+                                   static_cast<unsigned char*>(rc->sc.dots.get()) + std::size_t(s) * w * es, w * es,
+                                   cudaMemcpyDefault, st));
+    }
+}
+
+void check_transport(RankContext* rc) {
+    if (rc->transport != Transport::nccl || !rc->comm) return;
+    ncclResult_t as = ncclSuccess;
+    NCK(ncclCommGetAsyncError(rc->comm, &as));
+    if (as != ncclSuccess && as != ncclInProgress)
+        fail(errc::transport, std::string("NCCL asynchronous error: ") + ncclGetErrorString(as));
+}
+
+// a step may be captured when every host-side input is baked into device memory
+bool graphable(const SpmvOptions& o) {
+    if ((o.flags & kFlagVshift) && pointer_kind(o.gamma_list, nullptr) != MemKind::device) return false;
+    if ((o.flags & kFlagDots) && pointer_kind(o.dot, nullptr) != MemKind::device) return false;
+    return true;
+}
+
+bool capture_step(RankContext* rc, RankContext::Graph& g, DenseMat& y, const DenseMat& x, const SpmvOptions& o,
+                  DenseMat* z, bool nocomm) {
+    if (!rc->cap) {
+        CK(cudaStreamCreateWithFlags(&rc->cap, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&rc->cev_x, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&rc->cev_halo, cudaEventDisableTiming));
+    }
+    CK(cudaStreamBeginCapture(rc->cap, cudaStreamCaptureModeThreadLocal));
+    std::string why;
+    const std::uint64_t bytes0 = rc->bytes, msgs0 = rc->msgs;  // capturing moves no data
+    try {
+        rank_step(rc, y, x, o, z, nocomm, rc->cap, true);
+    } catch (const std::exception& e) {
+        why = e.what();
+    }
+    rc->bytes = bytes0;
+    rc->msgs = msgs0;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(rc->cap, &graph);
+    if (why.empty() && e != cudaSuccess) why = cudaGetErrorString(e);
+    cudaGraphExec_t exec = nullptr;
+    if (why.empty()) {
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        if (e != cudaSuccess) why = cudaGetErrorString(e);
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (!why.empty()) {
+        if (std::getenv("SELLKIT_VERBOSE"))
+            std::fprintf(stderr, "[sellkit] rank step not capturable (%s); running eagerly\n", why.c_str());
+        rc->graphs_broken = true;
+        return false;
+    }
+    g.exec = exec;
+    return true;
+}
+
+}  // namespace
 
 void rankctx_spmv(RankContext* rc, DenseMat& y, const DenseMat& x, const SpmvOptions& o, DenseMat* z, bool nocomm) {
     RankPart& part = rc->part;
     const RankPlan& p = part.plan;
     SK_REQUIRE(rc->sends_ready || nocomm || p.nranks == 1, errc::state, "send lists were not finalised");
-    SK_REQUIRE(rc->comm != nullptr || nocomm || p.nranks == 1, errc::state, "rank context is not connected");
+    SK_REQUIRE(rc->transport != Transport::none || nocomm || p.nranks == 1, errc::state,
+               "rank context is not connected");
     SK_REQUIRE(x.nrows == p.nrows && y.nrows == p.nrows && x.ncols == y.ncols, errc::shape_mismatch,
                "x and y must hold this rank's rows");
     SK_REQUIRE(x.mem == MemKind::device && y.mem == MemKind::device, errc::unsupported,
                "rank vectors must be device-resident");
+    SK_REQUIRE(y.data != x.data, errc::invalid_arg, "y must not alias x");
     const bool chain = (o.flags & kFlagChain) != 0;
     SK_REQUIRE(!chain || z != nullptr, errc::invalid_arg, "CHAIN_AXPBY requires z");
+    SK_REQUIRE(!chain || (z->mem == MemKind::device && z->same_shape(y)), errc::shape_mismatch,
+               "z must be a device block of y's shape");
     const std::uint32_t dots = o.flags & kFlagDots;
     SK_REQUIRE(!dots || o.dot != nullptr, errc::invalid_arg, "dot flags require a dot buffer");
+    SK_REQUIRE((o.flags & ~kFlagAll) == 0, errc::invalid_arg, "unknown spmv flag");
+    SK_REQUIRE(!((o.flags & kFlagShift) && (o.flags & kFlagVshift)), errc::invalid_arg,
+               "SHIFT and VSHIFT are mutually exclusive");
+    SK_REQUIRE(!(o.flags & kFlagVshift) || o.gamma_list != nullptr, errc::invalid_arg, "VSHIFT requires a gamma list");
     const lidx w = x.ncols;
-    const std::size_t es = value_bytes(p.dt);
+    SK_REQUIRE(rc->transport != Transport::ipc || w <= rc->ipc_max_w, errc::capacity,
+               "block width exceeds the IPC slots exported at connect time");
     DeviceGuard g(part.device);
     auto& rt = runtime(part.device);
-    ensure_scratch(rc->sc, part, w);
-    std::size_t mult = 1;
-    const ncclDataType_t nt = nccl_type(p.dt, mult);
-    const bool exchange = !nocomm && p.nranks > 1 && (!p.send_to.empty() || !p.recv_owner.empty());
-    if (exchange) {
-        CK(cudaEventRecord(part.ev_x, rt.stream));
-        CK(cudaStreamWaitEvent(part.comm, part.ev_x, 0));
-        CK(cudaStreamWaitEvent(part.comm, part.ev_done, 0));  // previous remote sweep consumed the halo
-        std::size_t off = 0;
-        std::vector<std::size_t> soff;
-        for (std::size_t s = 0; s < p.send_to.size(); ++s) {
-            const lidx cnt = lidx(p.send_local_rows[s].size());
-            soff.push_back(off);
-            visit_dt(p.dt, [&]<class T>() {
-                pack_kernel<T><<<pack_grid(gidx(cnt) * w), 256, 0, part.comm>>>(
-                    reinterpret_cast<const T*>(x.data), x.row_stride(), x.col_step(), part.send_rows[s].as<lidx>(),
-                    cnt, w, rc->sc.sendbuf.as<T>() + off);
-                return 0;
-            });
-            off += std::size_t(cnt) * w;
+    ensure_rank_buffers(rc, w);
+    bool done = false;
+    if (rc->graphs_on && !rc->graphs_broken && graphable(o)) {
+        const StepKey key = make_key(y, x, o, z, nocomm);
+        RankContext::Graph* hit = nullptr;
+        for (auto& gr : rc->graphs)
+            if (gr.key == key) hit = &gr;
+        if (hit && !hit->exec) capture_step(rc, *hit, y, x, o, z, nocomm);  // second use: capture
+        if (hit && hit->exec) {
+            CK(cudaGraphLaunch(hit->exec, rt.stream));
+            done = true;
+            // the transport counters advance as if the step ran eagerly
+            const bool exchange = !nocomm && p.nranks > 1 && (!p.send_to.empty() || !p.recv_owner.empty());
+            if (exchange) {
+                for (auto& rows : p.send_local_rows) rc->bytes += std::uint64_t(rows.size()) * w * value_bytes(p.dt);
+                rc->msgs += p.send_to.size();
+            }
+            if (dots && p.nranks > 1 && rc->transport != Transport::none) {
+                rc->msgs += 2 * std::uint64_t(p.nranks - 1);
+                rc->bytes += 2 * std::uint64_t(p.nranks - 1) * 3 * w * value_bytes(p.dt);
+            }
+        } else if (!hit) {
+            if (rc->graphs.size() >= 8) {
+                if (rc->graphs.front().exec) cudaGraphExecDestroy(rc->graphs.front().exec);
+                rc->graphs.erase(rc->graphs.begin());
+            }
+            rc->graphs.push_back(RankContext::Graph{key, nullptr});
         }
-        CK(cudaGetLastError());
-        NCK(ncclGroupStart());
-        for (std::size_t q = 0; q < p.recv_owner.size(); ++q)
-            NCK(ncclRecv(static_cast<unsigned char*>(rc->sc.halo.get()) + std::size_t(p.recv_offset[q]) * w * es,
-                         std::size_t(p.recv_count[q]) * w * mult, nt, p.recv_owner[q], rc->comm, part.comm));
-        for (std::size_t s = 0; s < p.send_to.size(); ++s) {
-            const std::size_t cnt = p.send_local_rows[s].size();
-            NCK(ncclSend(static_cast<unsigned char*>(rc->sc.sendbuf.get()) + soff[s] * es, cnt * w * mult, nt,
-                         p.send_to[s], rc->comm, part.comm));
-            rc->bytes += cnt * w * es;
-            rc->msgs += 1;
-        }
-        NCK(ncclGroupEnd());
-        CK(cudaEventRecord(part.ev_halo, part.comm));
     }
-    rank_sweeps(part, rc->sc, y, x, o, z, !exchange && (nocomm || p.recv_owner.empty()), rt.stream,
-                [&] { CK(cudaStreamWaitEvent(rt.stream, part.ev_halo, 0)); });
-    CK(cudaEventRecord(part.ev_done, rt.stream));
-    if (dots) {
-        void* res = rc->sc.dots.get();
-        if (p.nranks > 1 && rc->comm) {
-            if (rc->dots_all.bytes() < std::size_t(p.nranks) * 3 * w * es)
-                rc->dots_all = DeviceBuffer(std::size_t(p.nranks) * 3 * w * es, part.device);
-            NCK(ncclAllGather(rc->sc.dots.get(), rc->dots_all.get(), 3 * std::size_t(w) * mult, nt, rc->comm, rt.stream));
-            visit_dt(p.dt, [&]<class T>() {
-                rank_sum_kernel<T><<<(3 * w + 127) / 128, 128, 0, rt.stream>>>(rc->dots_all.as<T>(), p.nranks, 3 * w,
-                                                                              rc->sc.dots.as<T>());
-                return 0;
-            });
-            rc->msgs += 2 * std::uint64_t(p.nranks - 1);
-            rc->bytes += 2 * std::uint64_t(p.nranks - 1) * 3 * w * es;
-        }
-        for (int s = 0; s < 3; ++s)
-            if (o.flags & (kFlagDotYY << s))
-                CK(cudaMemcpyAsync(static_cast<unsigned char*>(o.dot) + std::size_t(s) * w * es,
-                                   static_cast<unsigned char*>(res) + std::size_t(s) * w * es, w * es, cudaMemcpyDefault,
-                                   rt.stream));
-    }
+    if (!done) rank_step(rc, y, x, o, z, nocomm, rt.stream, false);
+    check_transport(rc);
     finish(rt);
 }
+
+void rankctx_set_options(RankContext* rc, int graphs, int reserve_sms) {
+    if (graphs >= 0) {
+        rc->graphs_on = graphs != 0;
+        if (!rc->graphs_on) {
+            DeviceGuard g(rc->part.device);
+            CK(cudaDeviceSynchronize());
+            rc->drop_graphs();
+        }
+        rc->graphs_broken = false;
+    }
+    if (reserve_sms >= 0) {
+        rc->reserve_sms = reserve_sms;
+        DeviceGuard g(rc->part.device);
+        CK(cudaDeviceSynchronize());
+        rc->drop_graphs();
+    }
+}
+
+int rankctx_transport(RankContext* rc) { return int(rc->transport); }
 
 void rankctx_stats(RankContext* rc, std::uint64_t* bytes, std::uint64_t* msgs, lidx* n_halo, std::uint64_t* halo_rows,
                    gidx* local_nnz, gidx* remote_nnz) {
@@ -750,15 +1247,7 @@ void rankctx_stats(RankContext* rc, std::uint64_t* bytes, std::uint64_t* msgs, l
 
 const SellMat* rankctx_local(RankContext* rc) { return rc->part.local.get(); }
 
-void rankctx_destroy(RankContext* rc) {
-    if (!rc) return;
-    if (rc->comm) {
-        DeviceGuard g(rc->part.device);
-        cudaDeviceSynchronize();
-        ncclCommDestroy(rc->comm);
-    }
-    delete rc;
-}
+void rankctx_destroy(RankContext* rc) { delete rc; }
 
 }  // namespace skb
 
@@ -933,6 +1422,43 @@ sellkit_error sellkit_ext_rankctx_connect(sellkit_rankctx* rc, const void* id128
         sk::require(rc && id128, "null argument");
         sk::rankctx_finalize_sends(rc->p);
         if (sk::rankctx_plan(rc->p).nranks > 1) sk::rankctx_connect(rc->p, id128);
+    });
+}
+
+sellkit_error sellkit_ext_rankctx_ipc_export(sellkit_rankctx* rc, int max_width, void* blob, size_t* blob_bytes) {
+    return sk::guarded([&] {
+        sk::require(rc && blob_bytes, "null argument");
+        const std::size_t need = sk::rankctx_ipc_blob_bytes(rc->p);
+        if (!blob) {
+            *blob_bytes = need;
+            return;
+        }
+        SK_REQUIRE(*blob_bytes >= need, sk::errc::capacity, "IPC blob buffer too small");
+        sk::rankctx_finalize_sends(rc->p);
+        sk::rankctx_ipc_export(rc->p, max_width, blob);
+        *blob_bytes = need;
+    });
+}
+
+sellkit_error sellkit_ext_rankctx_ipc_connect(sellkit_rankctx* rc, const void* blobs, size_t blob_bytes) {
+    return sk::guarded([&] {
+        sk::require(rc && blobs, "null argument");
+        if (sk::rankctx_plan(rc->p).nranks == 1) return;
+        sk::rankctx_ipc_connect(rc->p, blobs, blob_bytes);
+    });
+}
+
+sellkit_error sellkit_ext_rankctx_transport(const sellkit_rankctx* rc, int* transport) {
+    return sk::guarded([&] {
+        sk::require(rc && transport, "null argument");
+        *transport = sk::rankctx_transport(rc->p);
+    });
+}
+
+sellkit_error sellkit_ext_rankctx_set_options(sellkit_rankctx* rc, int graphs, int reserve_sms) {
+    return sk::guarded([&] {
+        sk::require(rc != nullptr, "null handle");
+        sk::rankctx_set_options(rc->p, graphs, reserve_sms);
     });
 }
 

@@ -74,6 +74,7 @@ struct RankPart {
     std::vector<DeviceBuffer> send_rows;  // int32 stored rows per send list
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_x = nullptr, ev_halo = nullptr, ev_done = nullptr;
+    mutable std::vector<lidx> perm_host;  // original local row -> stored row (cached)
     RankPart() = default;
     RankPart(const RankPart&) = delete;
     ~RankPart();
@@ -98,6 +99,13 @@ struct DistContext {
     std::vector<RankScratch> scratch;
     bool record = false;
     std::uint64_t bytes = 0, msgs = 0;
+    DeviceBuffer dots_all;      // k x 3w dot partials on rank 0's device
+    int ndev = 1;
+    std::vector<char> peer_ok;  // [ndev x ndev]: peer access enabled from i to j
+    // may rank memory on `dst` be written by kernels running on `src`?
+    bool direct(int src, int dst) const {
+        return src == dst || (src < ndev && dst < ndev && peer_ok[std::size_t(src) * ndev + dst]);
+    }
 };
 
 struct DistVec {
@@ -115,7 +123,8 @@ void dist_gather(const DistContext& ctx, const DistVec& v, DenseMat& out);
 void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions& opts, int mode, DistVec* z,
                bool nocomm);
 
-// ------------------------------------------------ one process per GPU (NCCL)
+// ------------------------------------------ one process per GPU (NCCL or IPC)
+enum class Transport : int { none = 0, nccl = 1, ipc = 2 };
 struct RankContext;
 RankContext* rankctx_create(const Crs& rows, const std::vector<gidx>& row_offset, int rank, lidx C, lidx sigma);
 RankPlan& rankctx_plan(RankContext* rc);
@@ -127,5 +136,10 @@ void rankctx_stats(RankContext* rc, std::uint64_t* bytes, std::uint64_t* msgs, l
 const SellMat* rankctx_local(RankContext* rc);
 void rankctx_destroy(RankContext* rc);
 void nccl_unique_id(void* out128);
+std::size_t rankctx_ipc_blob_bytes(RankContext* rc);
+void rankctx_ipc_export(RankContext* rc, int max_width, void* blob);
+void rankctx_ipc_connect(RankContext* rc, const void* blobs, std::size_t blob_bytes);
+void rankctx_set_options(RankContext* rc, int graphs, int reserve_sms);
+int rankctx_transport(RankContext* rc);
 
 }  // namespace skb

@@ -43,10 +43,16 @@ sellkit_error guarded(F&& f) noexcept {
         return SELLKIT_OK;
     } catch (const Error& e) {
         if (std::getenv("SELLKIT_VERBOSE")) std::fprintf(stderr, "[sellkit] %s\n", e.what());
+        set_last_error(e.what());
         return static_cast<sellkit_error>(static_cast<int>(e.code()));
     } catch (const std::bad_alloc&) {
+        set_last_error("allocation failure");
         return SELLKIT_ERR_ALLOC;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return SELLKIT_ERR_INVALID_ARG;
     } catch (...) {
+        set_last_error("unknown exception");
         return SELLKIT_ERR_INVALID_ARG;
     }
 }

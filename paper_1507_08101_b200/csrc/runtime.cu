@@ -125,6 +125,12 @@ DeviceRuntime& runtime(int device) {
     return *rt;
 }
 
+namespace {
+thread_local std::string t_last_error;
+}
+void set_last_error(const char* msg) { t_last_error = msg ? msg : ""; }
+const char* last_error_message() { return t_last_error.c_str(); }
+
 bool sync_mode() { return g_sync; }
 void set_sync_mode(bool s) { g_sync = s; }
 

@@ -138,9 +138,18 @@ static bool spmv_host_streamed(DenseMat& y, const SellMat& A, const DenseMat& x,
         CK(cudaEventRecord(ev_in[s], rt.h2d));
         xdone = x1;
     }
+    // SHIFT/VSHIFT/DOT_XY/DOT_XX also read x at the block's own rows: those must be
+    // resident too, whatever the block's column watermark
+    const bool need_x = (o.flags & (kFlagShift | kFlagVshift | kFlagDotXY | kFlagDotXX)) != 0;
     for (int b = 0; b < nb; ++b) {
-        int s = 0;  // first slab that contains the block's watermark row
-        while (s < nb - 1 && std::min<gidx>(x.nrows, gidx(x.nrows) * (s + 1) / nb) <= gidx(A.watermark[b])) ++s;
+        gidx need = gidx(A.watermark[b]);  // largest x row the block reads
+        if (need_x) {
+            gidx r0, r1;
+            rows_of(b, r0, r1);
+            if (r1 > r0) need = std::max(need, std::min<gidx>(x.nrows, r1) - 1);
+        }
+        int s = 0;  // first slab that contains row `need`
+        while (s < nb - 1 && std::min<gidx>(x.nrows, gidx(x.nrows) * (s + 1) / nb) <= need) ++s;
         slab_for[b] = std::max(s, b);  // y/z inputs of block b arrive with slab b
     }
     const bool dots = (o.flags & kFlagDots) != 0;
@@ -221,6 +230,12 @@ KernelVariant select_kernel(lidx chunk_height, lidx block_width, Order order) {
     return {0, 0, false};
 }
 
+std::size_t spmv_scratch_bytes(Datatype dt, lidx width, int num_sms) {
+    const std::size_t W = std::size_t(width);
+    const std::size_t max_parts = std::size_t(num_sms) * 32 * ((W + kGW - 1) / kGW + 1);
+    return (W + 3 * W + max_parts * 3 * std::max<std::size_t>(W, kGW)) * value_bytes(dt) + 256;
+}
+
 void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& o, const SpmvHooks& hooks) {
     auto& rt = runtime(A.device);
     cudaStream_t st = hooks.stream ? hooks.stream : rt.stream;
@@ -277,9 +292,10 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         }
 
         // scratch: [gamma_list W][final dots 3W][partials]
-        const std::size_t max_parts = std::size_t(rt.num_sms) * 32 * std::size_t((W + kGW - 1) / kGW + 1);
-        const std::size_t need = (std::size_t(W) + 3 * W + max_parts * 3 * std::max<int>(W, kGW)) * es + 256;
-        auto* sc = static_cast<unsigned char*>(rt.scratch_bytes(need));
+        const std::size_t need = spmv_scratch_bytes(A.dt, W, rt.num_sms);
+        auto* sc = static_cast<unsigned char*>(hooks.scratch && hooks.scratch_size >= need ? hooks.scratch
+                                                                                        : rt.scratch_bytes(need));
+        if (hooks.reserve_sms > 0) a.grid_sms = std::max(1, rt.num_sms - hooks.reserve_sms);
         T* gl = reinterpret_cast<T*>(sc);
         T* res = gl + W;
         a.partial = res + 3 * W;

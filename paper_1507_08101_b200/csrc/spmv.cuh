@@ -53,7 +53,13 @@ struct SpmvHooks {
     cudaStream_t stream = nullptr; // override the runtime stream
     const DenseMat* x_self = nullptr;  // x of the output rows for shift/dots when x is a halo block
     gidx rg0 = 0, rg1 = -1;            // row groups (32 stored rows) to sweep; rg1 < 0: all
+    int reserve_sms = 0;               // leave this many SMs to concurrent work (halo pack)
+    void* scratch = nullptr;           // caller-owned device scratch (>= spmv_scratch_bytes);
+    std::size_t scratch_size = 0;      // else the runtime's shared scratch
 };
+
+// Device scratch one spmv_device call of width `width` needs (gamma list, dots, partials).
+std::size_t spmv_scratch_bytes(Datatype dt, lidx width, int num_sms);
 
 // Validation (spmv.hpp:98-125) + launch.  y/x/z may be host-resident views.
 void spmv(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& opts);

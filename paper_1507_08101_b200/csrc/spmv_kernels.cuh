@@ -30,6 +30,7 @@
 // groups in ascending order, so all SMs sweep the matrix front-to-back together
 // and the RHS window of a banded/stencil matrix stays L2-resident.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -70,6 +71,8 @@ struct KArgs {
     gidx rg0, rg1;  // row groups (32 stored rows each) [rg0, rg1) swept by this launch
     const int* sweep_order;  // full sweeps only: blocks of sweep_brg row groups in this order
     int sweep_brg;           // 0 = natural order
+    int grid_sms;            // launch: SMs the grid may fill (0 = all; the rest stay free for a
+                             // concurrent halo pack on the communication stream)
 };
 
 namespace spmv_detail {
@@ -897,8 +900,12 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 }
             }
             mbar_wait(&empty[s], (k & 1u) ^ 1u);
-            const gidx c0 = tile_rg(t) * (32 / C);
-            const gidx c1 = min(min(a.nchunks, a.rg1 * (32 / C)), c0 + chunks_per_tile);
+            // a partial last sweep-order block leaves tiles past the end: clamp their
+            // header reads to the chunk range (nc = 0), keep their row origin
+            const gidx cend = min(a.nchunks, a.rg1 * (32 / C));
+            const gidx c0u = tile_rg(t) * (32 / C);
+            const gidx c0 = min(c0u, cend);
+            const gidx c1 = min(cend, c0 + chunks_per_tile);
             const int nc = int(c1 - c0);
             const gidx off0 = a.chunk_offset[c0];
             for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
@@ -909,7 +916,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 hdr[s].overflow = fits ? 0 : 1;
                 hdr[s].nchunks = nc;
                 hdr[s].off0 = off0;
-                hdr[s].row0 = int(c0 / (32 / C)) * 32;
+                hdr[s].row0 = int(c0u / (32 / C)) * 32;
             }
             __syncwarp();
             if (lane == 0) {
@@ -928,8 +935,8 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             if constexpr (SK_HDR_PREFETCH > 0 && (PLAIN || DOTS)) {
                 const gidx tn = tile_of(it + SK_HDR_PREFETCH, seg);
                 if (tn < ntiles) {
-                    const gidx cn0 = tile_rg(tn) * (32 / C);
-                    const gidx cn1 = min(min(a.nchunks, a.rg1 * (32 / C)), cn0 + chunks_per_tile);
+                    const gidx cn0 = min(tile_rg(tn) * (32 / C), cend);
+                    const gidx cn1 = min(cend, cn0 + chunks_per_tile);
                     prefetch_headers(a.chunk_offset, a.chunk_len, cn0, int(cn1 - cn0), lane);
                 }
             }
@@ -1264,11 +1271,26 @@ __global__ void dot_final_kernel(const T* partial, int nparts, int W, int layout
 
 // ------------------------------------------------------------------ dispatch
 
+template <class T>
+inline int grid_sms_of(const KArgs<T>& a, const DeviceRuntime& rt) {
+    return a.grid_sms > 0 ? std::min(a.grid_sms, rt.num_sms) : rt.num_sms;
+}
+
 struct LaunchShape {
     int grid;
     int nparts;
     int layout;
 };
+
+// The dynamic shared-memory limit set by cudaFuncSetAttribute applies to the current
+// device only: set it once per (kernel, device), tracked in the caller's device mask.
+template <class K>
+void smem_attr_per_device(K kernel, std::size_t smem, int device, std::atomic<std::uint64_t>& devs) {
+    const std::uint64_t bit = device < 64 ? (std::uint64_t(1) << device) : 0;
+    if (bit && (devs.load(std::memory_order_acquire) & bit)) return;
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (bit) devs.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 template <class K>
 int occupancy_blocks(K kernel) {
@@ -1301,11 +1323,8 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
     using P = TPlan<T, W>;
     constexpr int U = unroll_of<T, P, SK_UBUDGET>();
     auto kern = spmv_tma_kernel<T, C, W, U>;
-    static bool attr = [&] {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tma_smem_bytes<T, W>())));
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<std::uint64_t> attr_devs{0};
+    smem_attr_per_device(kern, tma_smem_bytes<T, W>(), rt.device, attr_devs);
     static int per_sm = [&] {
         int nb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, tma_smem_bytes<T, W>()));
@@ -1313,7 +1332,7 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
     }();
     const gidx ngroups = a.rg1 - a.rg0;
     const gidx ntiles = (ngroups + rgt - 1) / rgt;
-    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * grid_sms_of(a, rt))));
     static const int seg = [] {
         const char* e = std::getenv("SELLKIT_TMA_SEG");
         return e ? std::max(1, std::atoi(e)) : 1;
@@ -1354,11 +1373,8 @@ LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaS
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
-    static bool attr = [&] {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<std::uint64_t> attr_devs{0};
+    smem_attr_per_device(kern, smem, rt.device, attr_devs);
     static int per_sm = [&] {
         int nb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kTmaThreads, smem));
@@ -1368,7 +1384,7 @@ LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaS
     // with a sweep order, tiles never straddle a block: blocks x (block / tile) tiles
     const gidx blocks = a.sweep_brg > 0 ? (ngroups + a.sweep_brg - 1) / a.sweep_brg : 0;
     const gidx ntiles = a.sweep_brg > 0 ? blocks * (a.sweep_brg / rgt) : (ngroups + rgt - 1) / rgt;
-    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * rt.num_sms)));
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(ntiles, gidx(per_sm) * grid_sms_of(a, rt))));
     static const int seg = [] {
         const char* e = std::getenv("SELLKIT_TMA_SEG");
         return e ? std::max(1, std::atoi(e)) : 1;
@@ -1419,7 +1435,7 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
     const gidx ngroups = a.rg1 - a.rg0;
     const gidx items = ngroups * P::NSLICE;
     const gidx need = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    const int grid = int(std::max<gidx>(1, std::min<gidx>(need, gidx(per_sm) * rt.num_sms)));
+    const int grid = int(std::max<gidx>(1, std::min<gidx>(need, gidx(per_sm) * grid_sms_of(a, rt))));
     kern<<<grid, kBlock, 0, st>>>(a);
     return {grid, grid, 0};
 }
@@ -1428,7 +1444,7 @@ template <class T>
 LaunchShape launch_generic(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st) {
     const int ncb = (a.width + kGW - 1) / kGW;
     const gidx need = ((a.rg1 - a.rg0) * 32 + kBlock - 1) / kBlock;
-    const int gx = int(std::max<gidx>(1, std::min<gidx>(need, gidx(rt.num_sms) * 8)));
+    const int gx = int(std::max<gidx>(1, std::min<gidx>(need, gidx(grid_sms_of(a, rt)) * 8)));
     spmv_generic_kernel<T><<<dim3(gx, ncb), kBlock, 0, st>>>(a);
     return {gx, gx, 1};
 }

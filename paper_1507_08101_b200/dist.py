@@ -213,6 +213,30 @@ class RankContext:
         buf = (C.c_char * 128).from_buffer_copy(nccl_id)
         self.sk.call("sellkit_ext_rankctx_connect", self.h, C.cast(buf, vp))
 
+    def ipc_export(self, max_width: int) -> bytes:
+        """Export this rank's IPC send slots / dot slot / flags (sellkit_ext_rankctx_ipc_export)."""
+        n = C.c_size_t(0)
+        self.sk.call("sellkit_ext_rankctx_ipc_export", self.h, max_width, None, C.byref(n))
+        buf = (C.c_char * n.value)()
+        self.sk.call("sellkit_ext_rankctx_ipc_export", self.h, max_width, C.cast(buf, vp), C.byref(n))
+        return bytes(buf.raw)
+
+    def ipc_connect(self, blobs: List[bytes]):
+        """Open every rank's exported buffers (blobs in rank order)."""
+        size = len(blobs[0])
+        assert all(len(b) == size for b in blobs) and len(blobs) == self.world
+        raw = (C.c_char * (size * len(blobs))).from_buffer_copy(b"".join(blobs))
+        self.sk.call("sellkit_ext_rankctx_ipc_connect", self.h, C.cast(raw, vp), size)
+
+    @property
+    def transport(self) -> str:
+        t = C.c_int()
+        self.sk.call("sellkit_ext_rankctx_transport", self.h, C.byref(t))
+        return {0: "none", 1: "nccl", 2: "ipc"}[t.value]
+
+    def set_options(self, graphs: int = -1, reserve_sms: int = -1):
+        self.sk.call("sellkit_ext_rankctx_set_options", self.h, graphs, reserve_sms)
+
     def row_perm(self) -> np.ndarray:
         out = np.zeros(self.nrows, np.int32)
         self.sk.call("sellkit_ext_rankctx_row_perm", self.h, _ptr(out))
@@ -256,23 +280,47 @@ class RankContext:
             pass
 
 
+def default_transport(world: int) -> str:
+    """IPC when every rank runs on this node (torchrun's LOCAL_WORLD_SIZE), else NCCL;
+    SELLKIT_HALO_TRANSPORT=ipc|nccl overrides."""
+    import os
+    t = os.environ.get("SELLKIT_HALO_TRANSPORT", "auto")
+    if t != "auto":
+        return t
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    return "ipc" if local == world else "nccl"
+
+
 def setup_rank(sk: Sellkit, rows_crs, row_offsets, rank: int, world: int, chunk_height: int, sigma: int,
-               group=None) -> RankContext:
-    """Build this rank's parts, exchange halo requests, connect NCCL."""
+               group=None, transport: Optional[str] = None, max_width: int = 64) -> RankContext:
+    """Build this rank's parts, exchange halo requests, connect the halo transport.
+
+    transport: "ipc" (CUDA-IPC slots + copy-engine pulls, one node) or "nccl"
+    (send/recv over NCCL); default :func:`default_transport`.  Only the setup
+    handshake (requests, IPC blobs / NCCL id) goes through ``torch.distributed``."""
     import torch.distributed as tdist
     rc = RankContext(sk, rows_crs, row_offsets, rank, chunk_height, sigma)
     if world > 1:
         incoming = exchange_requests(rc.requests(), rank, world, group)
         for to in sorted(incoming):
             rc.set_sends(to, incoming[to])
-        idbuf = bytearray(128)
-        if rank == 0:
-            raw = (C.c_char * 128)()
-            sk.call("sellkit_ext_nccl_unique_id", C.cast(raw, vp))
-            idbuf = bytearray(raw.raw)
-        obj = [bytes(idbuf)]
-        tdist.broadcast_object_list(obj, src=0, group=group)
-        rc.connect(obj[0])
+        transport = transport or default_transport(world)
+        if transport == "ipc":
+            blobs: List[Optional[bytes]] = [None] * world
+            tdist.all_gather_object(blobs, rc.ipc_export(max_width), group=group)
+            rc.ipc_connect(blobs)
+        elif transport == "nccl":
+            idbuf = bytearray(128)
+            if rank == 0:
+                raw = (C.c_char * 128)()
+                sk.call("sellkit_ext_nccl_unique_id", C.cast(raw, vp))
+                idbuf = bytearray(raw.raw)
+            obj = [bytes(idbuf)]
+            tdist.broadcast_object_list(obj, src=0, group=group)
+            rc.connect(obj[0])
+        else:
+            raise ValueError(f"unknown halo transport {transport!r}")
+        tdist.barrier(group=group)  # every rank connected before the first step
     else:
         rc.connect(bytes(128))
     return rc
@@ -297,7 +345,8 @@ class BenchJob:
         return float(np.mean(per_step))
 
 
-def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank: int, world: int) -> BenchJob:
+def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank: int, world: int,
+                transport: Optional[str] = None) -> BenchJob:
     """This rank's z-slab of the n^3 7-point stencil (BY_ROWS, equal weights), x hashed on the device."""
     import torch
     N = n ** 3
@@ -305,7 +354,7 @@ def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank
     r0, r1 = int(off[rank]), int(off[rank + 1])
     rows = sk.crs_stencil(7, n, r0, r1)
     _, _, nnz_local = rows.dims()
-    rc = setup_rank(sk, rows, off, rank, world, chunk_height, sigma)
+    rc = setup_rank(sk, rows, off, rank, world, chunk_height, sigma, transport=transport, max_width=w)
     del rows
     nloc = r1 - r0
     # rank vectors in HBM (torch allocations viewed by the library: the e2e copies below

@@ -41,9 +41,10 @@ ROW_FN = C.CFUNCTYPE(C.c_int, gidx, C.POINTER(lidx), C.POINTER(gidx), vp, vp)
 
 
 class SellkitError(RuntimeError):
-    def __init__(self, code: int, where: str, name: str = ""):
-        super().__init__(f"{where} failed: sellkit_error {code} ({name})")
+    def __init__(self, code: int, where: str, name: str = "", detail: str = ""):
+        super().__init__(f"{where} failed: sellkit_error {code} ({name})" + (f": {detail}" if detail else ""))
         self.code = code
+        self.detail = detail
 
 
 class spmv_opts(C.Structure):
@@ -142,6 +143,7 @@ _API = [
 
 # include/sellkit_ext.h (B200 library only)
 _EXT = [
+    ("sellkit_ext_last_error", C.c_char_p, []),
     ("sellkit_ext_set_sync", err_t, [C.c_int]),
     ("sellkit_ext_synchronize", err_t, []),
     ("sellkit_ext_stream", err_t, [C.POINTER(vp)]),
@@ -163,6 +165,10 @@ _EXT = [
     ("sellkit_ext_rankctx_set_sends", err_t, [vp, C.c_int, vp, lidx]),
     ("sellkit_ext_rankctx_send", err_t, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(lidx), vp]),
     ("sellkit_ext_rankctx_connect", err_t, [vp, vp]),
+    ("sellkit_ext_rankctx_ipc_export", err_t, [vp, C.c_int, vp, C.POINTER(C.c_size_t)]),
+    ("sellkit_ext_rankctx_ipc_connect", err_t, [vp, vp, C.c_size_t]),
+    ("sellkit_ext_rankctx_transport", err_t, [vp, C.POINTER(C.c_int)]),
+    ("sellkit_ext_rankctx_set_options", err_t, [vp, C.c_int, C.c_int]),
     ("sellkit_ext_rank_spmv", err_t, [vp, vp, vp, C.POINTER(spmv_opts), vp, C.c_int]),
     ("sellkit_ext_rankctx_stats", err_t, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(lidx),
                                           C.POINTER(C.c_uint64), C.POINTER(gidx), C.POINTER(gidx)]),
@@ -214,7 +220,10 @@ class Sellkit:
     # -- plumbing -----------------------------------------------------------
     def check(self, code: int, where: str):
         if code != OK:
-            raise SellkitError(code, where, self.lib.sellkit_error_name(code).decode())
+            detail = ""
+            if self.has_ext:
+                detail = (self.lib.sellkit_ext_last_error() or b"").decode(errors="replace")
+            raise SellkitError(code, where, self.lib.sellkit_error_name(code).decode(), detail)
 
     def call(self, name: str, *args):
         """Call `name`; handle objects may be passed directly and stay alive for the call."""

@@ -185,6 +185,9 @@ def gen_tsm():
     print("tsm.npz:", len(out), "arrays")
 
 
+from fused_cases import FUSED as FUSED_DIST  # noqa: E402  (name, flags, gamma)
+
+
 def gen_dist(mats):
     out = {}
     ref = ref_lib()
@@ -228,6 +231,32 @@ def gen_dist(mats):
             ref.call("sellkit_ctx_comm_stats", ctx, sk.C.byref(bytes_), sk.C.byref(msgs))
             out[f"{key}|x"], out[f"{key}|y"], out[f"{key}|dot"] = xv, yg.copy_out(), dots
             out[f"{key}|comm"] = np.array([bytes_.value, msgs.value], np.int64)
+            # fused flags through dist_spmv (own RNG stream: the arrays above stay as they were)
+            for fname, flags, gam in FUSED_DIST:
+                frng = np.random.default_rng(1000 + 31 * k + sum(map(ord, name)) + (0 if fname == "f1" else 7))
+                x2, y0, z0 = (frng.uniform(-1, 1, (len(m[0]) - 1, w)) for _ in range(3))
+                dz = sk.vp()
+                ref.call("sellkit_dvec_create", ctx, w, 0, sk.C.byref(dz))
+                gx2, gy0, gz0 = ref.densemat_from(x2), ref.densemat_from(y0), ref.densemat_from(z0)
+                ref.call("sellkit_dvec_scatter", ctx, gx2.h, dx)
+                ref.call("sellkit_dvec_scatter", ctx, gy0.h, dy)
+                ref.call("sellkit_dvec_scatter", ctx, gz0.h, dz)
+                sc = {nm: np.array(vv, np.float64) for nm, vv in
+                      [("alpha", [0.5]), ("beta", [-1.0]), ("delta", [1.0]), ("eta", [0.3]), ("gamma", gam)]}
+                fo = sk.spmv_opts()
+                fo.flags = flags
+                fo.alpha, fo.beta, fo.delta, fo.eta, fo.gamma = (sc[nm].ctypes.data for nm in
+                                                                 ("alpha", "beta", "delta", "eta", "gamma"))
+                fdots = np.zeros(3 * w)
+                fo.dot = fdots.ctypes.data
+                ref.call("sellkit_dist_spmv", dy, ctx, dx, sk.C.byref(fo), 0, dz, 1)
+                zg = ref.densemat(len(m[0]) - 1, w)
+                ref.call("sellkit_dvec_gather", ctx, dy, yg.h)
+                ref.call("sellkit_dvec_gather", ctx, dz, zg.h)
+                fk = f"{key}|{fname}"
+                out[fk + "|x"], out[fk + "|y0"], out[fk + "|z0"] = x2, y0, z0
+                out[fk + "|y"], out[fk + "|z"], out[fk + "|dot"] = yg.copy_out(), zg.copy_out(), fdots
+                ref.lib.sellkit_dvec_destroy(dz)
             ref.lib.sellkit_dvec_destroy(dx)
             ref.lib.sellkit_dvec_destroy(dy)
             ref.lib.sellkit_ctx_destroy(ctx)

@@ -46,6 +46,43 @@ def test_dist_vs_reference_golden(sk, golden):
         assert list(ctx.comm_stats()) == g[key + "|comm"].tolist(), key  # byte/message counts exact
 
 
+def test_dist_fused_vs_reference_golden(sk, golden):
+    """The fused golden cases (shift / vshift, AXPBY, chain, dots) of the reference's own
+    dist_spmv: y and z bit for bit, dots within 1e-12 (single process, all ranks here)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from fused_cases import FUSED
+    g = golden("dist.npz")
+    cases = sorted({tuple(k.split("|")[:5]) for k in g.files if "|crs|" not in k})
+    w = 2
+    for name, k, by_nnz, C, sigma in cases:
+        key = f"{name}|{k}|{by_nnz}|{C}|{sigma}"
+        rp, c, v = g[f"{name}|crs|rowptr"], g[f"{name}|crs|col"], g[f"{name}|crs|val"]
+        n = len(rp) - 1
+        ctx = dist.DistContext(sk, sk.crs(rp, c, v), int(k), int(C), int(sigma), by_nnz=bool(int(by_nnz)))
+        dx, dy, dz = ctx.vec(w), ctx.vec(w), ctx.vec(w)
+        for fname, flags, gam in FUSED:
+            fk = f"{key}|{fname}"
+            for arr, dv in [(g[fk + "|x"], dx), (g[fk + "|y0"], dy), (g[fk + "|z0"], dz)]:
+                ctx.scatter(sk.densemat_from(arr), dv)
+            dots = np.zeros(3 * w)
+            ctx.spmv(dy, dx, flags=flags, alpha=0.5, beta=-1.0, gamma=gam if len(gam) > 1 else gam[0], delta=1.0,
+                     eta=0.3, z=dz, dot=dots)
+            yg, zg = sk.densemat(n, w), sk.densemat(n, w)
+            ctx.gather(dy, yg)
+            ctx.gather(dz, zg)
+            y = yg.copy_out()
+            assert np.array_equal(y, g[fk + "|y"]), fk
+            assert np.array_equal(zg.copy_out(), g[fk + "|z"]), fk
+            xv = g[fk + "|x"]
+            sc = np.concatenate([np.sum(y ** 2, 0), np.sum(np.abs(xv * y), 0), np.sum(xv ** 2, 0)])
+            for s in range(3):
+                if flags & (sellkit.DOT_YY << s):
+                    part = slice(s * w, (s + 1) * w)
+                    assert np.all(np.abs(dots[part] - g[fk + "|dot"][part]) <= 1e-12 * (1 + sc[part])), fk
+
+
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 7, 8])
 @pytest.mark.parametrize("mode", [sellkit.NO_OVERLAP, sellkit.NAIVE_OVERLAP, sellkit.TASK_OVERLAP])
 def test_dist_fused_vs_serial(sk, orc, k, mode):

@@ -247,6 +247,41 @@ def test_streamed_pinned_host_buffers(sk, orc, w):
     assert np.all(np.abs(dots[:2 * w] - do[:2 * w]) <= 1e-12 * (1 + np.abs(do[:2 * w])))
 
 
+@pytest.mark.parametrize("w", [1, 4])
+def test_streamed_pinned_strictly_lower(sk, orc, w):
+    """Streamed pinned-host spmv with x read at the block's own rows (SHIFT, <x,y>,
+    <x,x>) on a matrix whose rows only reach columns BELOW them (strictly lower, many
+    empty rows): a block's column watermark is then smaller than its own rows, so the
+    x slab holding those rows must also have arrived (spmv.cu streamed path)."""
+    import torch
+    rng = np.random.default_rng(77 + w)
+    n = 20000
+    rows, rp = [], [0]
+    for r in range(n):
+        k = 0 if (r % 97) > 60 or r == 0 else int(rng.integers(1, 4))
+        c = np.sort(rng.choice(max(1, min(r, 64)), size=min(k, max(1, min(r, 64))), replace=False)) if k else []
+        rows.append(np.asarray(c, np.int64))
+        rp.append(rp[-1] + len(c))
+    rp = np.array(rp, np.int64)
+    col = np.concatenate(rows).astype(np.int64)
+    val = rng.uniform(-1, 1, len(col))
+    A = sk.crs(rp, col, val).build(32, 1)
+    Ao = orc.build(rp, col, val, 32, 1)
+    xv, y0 = hash_block(n, w, 21), hash_block(n, w, 22)
+    bufs = {}
+    for name, arr in [("x", xv), ("y", y0)]:
+        t = torch.empty((n, w), dtype=torch.float64, pin_memory=True)
+        t.copy_(torch.from_numpy(arr))
+        bufs[name] = t
+    views = {k: sk.view_plain(t.data_ptr(), n * w, n, w, w, keep=t) for k, t in bufs.items()}
+    flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_XY | sellkit.DOT_XX
+    dots = np.zeros(3 * w)
+    sk.spmv(views["y"], A, views["x"], flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, dot=dots)
+    yo, _, do = orc.spmv(Ao, xv, y0, None, flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    assert np.array_equal(bufs["y"].numpy(), yo)
+    assert np.all(np.abs(dots[w:] - do[w:]) <= 1e-12 * (1 + np.abs(do[w:])))
+
+
 def test_spmv_validation(sk):
     I = sk.crs(np.arange(4), np.arange(3), np.ones(3)).build(1, 1)
     x, y = sk.densemat(3, 1), sk.densemat(3, 1)
