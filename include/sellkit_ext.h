@@ -68,10 +68,28 @@ sellkit_error sellkit_ext_mat_export(const sellkit_mat* m, int32_t* row_perm_inv
  * of block_rows (a multiple of 32) and swept in the order order[0..nblocks) (a
  * permutation of the block indices, nblocks = ceil(nrows_padded / block_rows)).
  * Used to keep the RHS reuse window small for matrices whose coupling distance is
- * long in row order (e.g. a pencil order over a 3-D lattice).  order == NULL
- * restores the natural order. */
+ * long in row order (e.g. a pencil order over a 3-D lattice).
+ * By default (and after order == NULL with block_rows == 0) the library picks the
+ * order itself: when the coupling distance (median farthest |column - row|) times the
+ * bytes a row streams exceeds half the L2, rows are swept in slabs walked along that
+ * distance (SELLKIT_AUTO_ORDER=0 disables it).  order == NULL with block_rows > 0
+ * forces the natural row order. */
 sellkit_error sellkit_ext_mat_set_sweep_order(sellkit_mat* m, sellkit_lidx block_rows, const int32_t* order,
                                               sellkit_gidx nblocks);
+
+/* Matrix-free operator (reference SellMatrix::apply_override, sellcs.hpp:116-119;
+ * spmv.hpp:131-135): once set, sellkit_spmv on this matrix validates its arguments as
+ * usual and then calls fn(y, x, opts, stream, ctx) instead of the built-in multiply.
+ * y and x are in storage index space; opts is the caller's (or the defaults when the
+ * caller passed NULL) and the override must honour the full fused contract.  `stream`
+ * is the library's cudaStream_t of the matrix's device: device work the override
+ * enqueues there (its own kernels, or library calls, which use that stream) is ordered
+ * with the caller's other library calls, and sellkit_spmv synchronises it before
+ * returning in the default synchronous mode.  A non-OK return is passed through.
+ * fn == NULL removes the override. */
+typedef sellkit_error (*sellkit_ext_apply_fn)(sellkit_densemat* y, const sellkit_densemat* x,
+                                              const sellkit_spmv_opts* opts, void* stream, void* ctx);
+sellkit_error sellkit_ext_mat_set_apply_override(sellkit_mat* m, sellkit_ext_apply_fn fn, void* ctx);
 
 /* ------------------------------------------------------- dense matrices -- */
 sellkit_error sellkit_ext_densemat_storage(const sellkit_densemat* m, void** data, sellkit_lidx* stride,

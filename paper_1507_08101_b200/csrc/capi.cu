@@ -459,7 +459,27 @@ sellkit_error sellkit_spmv(sellkit_densemat* y, const sellkit_mat* a, const sell
         } else {
             sk::spmv_options_from(y->m.dt, 0, nullptr, nullptr, nullptr, nullptr, nullptr, o);
         }
+        if (a->apply_override) {
+            // spmv.hpp:131-135: validate, then hand the whole fused operation to the override
+            sk::spmv_validate(y->m, *a->p, x->m, o);
+            sellkit_spmv_opts dflt;
+            sellkit_spmv_opts_init(&dflt);
+            sk::DeviceGuard g(a->p->device);
+            auto& rt = sk::runtime(a->p->device);
+            const sellkit_error e = a->apply_override(y, x, opts ? opts : &dflt, rt.stream, a->apply_ctx);
+            SK_REQUIRE(e == SELLKIT_OK, static_cast<sk::errc>(int(e)), "apply override failed");
+            sk::finish(rt);
+            return;
+        }
         sk::spmv(y->m, *a->p, x->m, o);
+    });
+}
+
+sellkit_error sellkit_ext_mat_set_apply_override(sellkit_mat* m, sellkit_ext_apply_fn fn, void* ctx) {
+    return guarded([&] {
+        require(m != nullptr, "null handle");
+        m->apply_override = fn;
+        m->apply_ctx = fn ? ctx : nullptr;
     });
 }
 
@@ -706,9 +726,11 @@ sellkit_error sellkit_ext_mat_set_sweep_order(sellkit_mat* m, sellkit_lidx block
         require(m != nullptr, "null handle");
         auto& a = *m->p;
         if (!order) {
+            // block_rows == 0: back to the automatic locality order; otherwise natural row order
             a.sweep_order = sk::DeviceBuffer();
             a.sweep_block_rgs = 0;
             a.sweep_blocks = 0;
+            a.sweep_policy = block_rows == 0 ? 0 : 1;
             return;
         }
         SK_REQUIRE(block_rows > 0 && block_rows % 32 == 0 && block_rows <= 32 * 4096, sk::errc::invalid_arg,
@@ -729,6 +751,7 @@ sellkit_error sellkit_ext_mat_set_sweep_order(sellkit_mat* m, sellkit_lidx block
         a.sweep_order = std::move(buf);
         a.sweep_block_rgs = int(block_rows / 32);
         a.sweep_blocks = nblocks;
+        a.sweep_policy = 2;
     });
 }
 

@@ -15,6 +15,9 @@ struct sellkit_crs {
 };
 struct sellkit_mat {
     std::unique_ptr<skb::SellMat> p;
+    // matrix-free replacement of the multiply (sellcs.hpp:116-119 apply_override)
+    sellkit_ext_apply_fn apply_override = nullptr;
+    void* apply_ctx = nullptr;
 };
 struct sellkit_densemat {
     skb::DenseMat m;

@@ -54,6 +54,19 @@ struct SellMat {
     DeviceBuffer sweep_order;   // int32 [sweep_blocks]
     int sweep_block_rgs = 0;
     gidx sweep_blocks = 0;
+    // sweep policy: 0 = automatic locality order (spmv.cu), 1 = natural row order,
+    // 2 = the caller's order above
+    int sweep_policy = 0;
+    // automatic order: coupling distance (median over row groups of the farthest
+    // |column - row| in stored space; -1 = not yet measured, 0 = not applicable) and
+    // the orders built so far, per slab size in blocks
+    mutable gidx coupling = -1;
+    struct AutoOrder {
+        int slab_blocks = 0;
+        gidx nblocks = 0;
+        DeviceBuffer order;  // int32 [nblocks]; empty: natural order is as good
+    };
+    mutable std::vector<AutoOrder> auto_orders;
     // streamed host-buffer spmv: largest column index per row-group block (lazily computed)
     mutable std::vector<lidx> watermark;
     mutable int watermark_blocks = 0;

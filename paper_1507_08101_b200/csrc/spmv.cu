@@ -2,6 +2,8 @@
 // host-resident vectors, kernel dispatch and the ordered dot reduction.
 #include "spmv_kernels.cuh"
 
+#include <algorithm>
+
 namespace skb {
 
 using namespace spmv_detail;
@@ -45,7 +47,105 @@ bool pinned_host(const DenseMat& m) {
     return attr.type == cudaMemoryTypeHost;
 }
 
+// farthest |column - stored row| over the real entries of each row group (32 stored rows)
+__global__ void coupling_kernel(const lidx* col, const gidx* chunk_offset, const lidx* rowlen, lidx C, lidx nrows,
+                                gidx ngroups, lidx* out) {
+    const gidx g = blockIdx.x * gidx(blockDim.x / 32) + threadIdx.x / 32;
+    if (g >= ngroups) return;
+    const int lane = threadIdx.x & 31;
+    const lidx row = lidx(g * 32 + lane);
+    lidx m = 0;
+    if (row < nrows) {
+        const gidx c = row / C;
+        const int i = row - lidx(c * C);
+        const gidx off = chunk_offset[c] + i;
+        const lidx len = rowlen[row];
+        for (lidx j = 0; j < len; ++j) {
+            const lidx d = col[off + gidx(j) * C] - row;
+            m = max(m, d < 0 ? -d : d);
+        }
+    }
+    m = lidx(__reduce_max_sync(0xffffffffu, unsigned(m)));
+    if (lane == 0) out[g] = m;
+}
+
+// Coupling distance of a square matrix swept by the row-contiguous kernels: the median
+// over row groups of the farthest |column - row| (a lattice's largest stride).
+gidx coupling_distance(const SellMat& A) {
+    if (A.coupling >= 0) return A.coupling;
+    A.coupling = 0;
+    if (A.nrows != A.ncols || A.nrows < 64 || A.C > 32 || 32 % A.C != 0) return 0;
+    auto& rt = runtime(A.device);
+    const gidx ngroups = (gidx(A.nrows) + 31) / 32;
+    DeviceBuffer d(std::size_t(ngroups) * sizeof(lidx), A.device);
+    coupling_kernel<<<int((ngroups + 7) / 8), 256, 0, rt.stream>>>(A.col.as<lidx>(), A.chunk_offset.as<gidx>(),
+                                                                    A.rowlen.as<lidx>(), A.C, A.nrows, ngroups,
+                                                                    d.as<lidx>());
+    CK(cudaGetLastError());
+    std::vector<lidx> h(static_cast<std::size_t>(ngroups));
+    CK(cudaMemcpyAsync(h.data(), d.get(), h.size() * sizeof(lidx), cudaMemcpyDeviceToHost, rt.stream));
+    CK(cudaStreamSynchronize(rt.stream));
+    std::nth_element(h.begin(), h.begin() + h.size() / 2, h.end());
+    A.coupling = h[h.size() / 2];
+    return A.coupling;
+}
+
 }  // namespace
+
+// Automatic locality order of a full sweep (no caller order): a row-ordered sweep
+// re-reads x[r + D] from HBM when the coupling distance D times the bytes streamed
+// per row (x row, matrix entries, y / z rows) exceeds what L2 keeps -- the z-plane
+// reuse of a 3-D lattice (C3: D = 131072 rows, 135 MB at w = 16 complex).  Then the
+// rows are swept in slabs walked along D: for each slab offset p, blocks p, p + D,
+// p + 2D, ... (a "pencil" through the lattice), so x[r + D] is reused a slab later.
+// The slab is sized so that three slabs of streams (planes z-1, z, z+1) fit a quarter
+// of L2.  Returns the device order and its block size in row groups, or nullptr.
+static const int* auto_sweep_order(const SellMat& A, lidx w, std::uint32_t flags, int& block_rgs, gidx& nblocks) {
+    const char* e_off = std::getenv("SELLKIT_AUTO_ORDER");
+    if ((e_off && std::string(e_off) == "0") || A.sweep_policy != 0) return nullptr;
+    const gidx D = coupling_distance(A);
+    if (D <= 0) return nullptr;
+    auto& rt = runtime(A.device);
+    const double es = double(value_bytes(A.dt));
+    const double nnz_row = double(A.nnz) / double(std::max<lidx>(1, A.nrows));
+    const double vec = es * w;
+    const double row_bytes = vec + nnz_row * (es + 4.0) + vec * (1.0 + ((flags & kFlagAxpby) ? 1.0 : 0.0) +
+                                                                 ((flags & kFlagChain) ? 2.0 : 0.0));
+    const char* e_l2 = std::getenv("SELLKIT_AUTO_ORDER_L2");  // cache size the decision assumes (tests)
+    const double l2 = e_l2 ? std::atof(e_l2) : double(rt.l2_bytes);
+    if (double(D) * row_bytes <= 0.5 * l2) return nullptr;  // the reuse window already fits L2
+    constexpr int kBlockRgs = 8;                              // 256-row blocks
+    const gidx brows = 32 * kBlockRgs;
+    const gidx Db = std::max<gidx>(1, (D + brows / 2) / brows);  // plane stride in blocks
+    const gidx slab_rows = gidx(0.25 * l2 / (3.0 * row_bytes));
+    const int Sb = int(std::max<gidx>(1, slab_rows / brows));
+    block_rgs = kBlockRgs;
+    nblocks = (gidx(A.nrows_padded) + brows - 1) / brows;
+    for (auto& o : A.auto_orders)
+        if (o.slab_blocks == Sb && o.nblocks == nblocks) return o.order.get() ? o.order.as<int>() : nullptr;
+    SellMat::AutoOrder ao;
+    ao.slab_blocks = Sb;
+    ao.nblocks = nblocks;
+    if (Sb < Db) {
+        std::vector<int> ord;
+        ord.reserve(std::size_t(nblocks));
+        const gidx planes = (nblocks + Db - 1) / Db;
+        for (gidx p0 = 0; p0 < Db; p0 += Sb)
+            for (gidx q = 0; q < planes; ++q)
+                for (gidx p = p0; p < std::min<gidx>(p0 + Sb, Db); ++p) {
+                    const gidx b = q * Db + p;
+                    if (b < nblocks) ord.push_back(int(b));
+                }
+        ao.order = DeviceBuffer(ord.size() * sizeof(int), A.device);
+        CK(cudaMemcpyAsync(ao.order.get(), ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice, rt.stream));
+        CK(cudaStreamSynchronize(rt.stream));
+        if (std::getenv("SELLKIT_VERBOSE"))
+            std::fprintf(stderr, "[sellkit] auto sweep order: coupling %lld rows, %.0f B/row, slabs of %d x 256 rows\n",
+                         (long long)D, row_bytes, Sb);
+    }
+    A.auto_orders.push_back(std::move(ao));
+    return A.auto_orders.back().order.get() ? A.auto_orders.back().order.as<int>() : nullptr;
+}
 
 // Streamed spmv on pinned host buffers: x arrives in row slabs on one copy engine,
 // each block of row groups is swept as soon as the x rows up to its largest column
@@ -286,9 +386,18 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         a.row_map = hooks.row_map;
         a.rg0 = hooks.rg0;
         a.rg1 = hooks.rg1 < 0 ? (gidx(A.nrows_padded) + 31) / 32 : hooks.rg1;
-        if (A.sweep_block_rgs > 0 && hooks.rg0 == 0 && hooks.rg1 < 0 && hooks.row_map == nullptr) {
-            a.sweep_order = A.sweep_order.as<int>();  // full sweep: the matrix's block order
-            a.sweep_brg = A.sweep_block_rgs;
+        if (hooks.rg0 == 0 && hooks.rg1 < 0 && hooks.row_map == nullptr) {  // full sweep
+            if (A.sweep_policy == 2 && A.sweep_block_rgs > 0) {
+                a.sweep_order = A.sweep_order.as<int>();  // the caller's block order
+                a.sweep_brg = A.sweep_block_rgs;
+            } else if (spec && A.sweep_policy == 0) {
+                int brg = 0;
+                gidx nb = 0;
+                if (const int* ord = auto_sweep_order(A, W, o.flags, brg, nb)) {
+                    a.sweep_order = ord;
+                    a.sweep_brg = brg;
+                }
+            }
         }
 
         // scratch: [gamma_list W][final dots 3W][partials]
@@ -321,9 +430,8 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
     });
 }
 
-// spmv.hpp:98-125 + 129-202
-void spmv(DenseMat& y, const SellMat& A, const DenseMat& x_in, const SpmvOptions& o) {
-    DenseMat x = x_in;
+// spmv.hpp:98-125
+void spmv_validate(const DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& o) {
     SK_REQUIRE(!y.scattered() && !x.scattered(), errc::unsupported,
                "scattered views are not supported by spmv; make a compact clone first");
     SK_REQUIRE(x.nrows == A.ncols, errc::shape_mismatch, "x rows must equal matrix columns");
@@ -346,7 +454,13 @@ void spmv(DenseMat& y, const SellMat& A, const DenseMat& x_in, const SpmvOptions
     }
     SK_REQUIRE(x.dt == A.dt && y.dt == A.dt && (!o.z || o.z->dt == A.dt), errc::invalid_arg,
                "datatype mismatch between y and A");
+}
 
+// spmv.hpp:129-202
+void spmv(DenseMat& y, const SellMat& A, const DenseMat& x_in, const SpmvOptions& o) {
+    DenseMat x = x_in;
+    spmv_validate(y, A, x, o);
+    const auto f = o.flags;
     DeviceGuard g(A.device);
     auto& rt = runtime(A.device);
     if (x.mem == MemKind::host && y.mem == MemKind::host && spmv_host_streamed(y, A, x, o)) return;

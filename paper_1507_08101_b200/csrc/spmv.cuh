@@ -61,6 +61,8 @@ struct SpmvHooks {
 // Device scratch one spmv_device call of width `width` needs (gamma list, dots, partials).
 std::size_t spmv_scratch_bytes(Datatype dt, lidx width, int num_sms);
 
+// Validation only (spmv.hpp:98-125): throws the reference's error codes.
+void spmv_validate(const DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& opts);
 // Validation (spmv.hpp:98-125) + launch.  y/x/z may be host-resident views.
 void spmv(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& opts);
 // Device-only entry used by the distributed path (no validation, no staging).

@@ -679,6 +679,63 @@ __device__ __forceinline__ void slot_add(T* p, T v) {
     *p = Ops<T>::add(*p, v);
 }
 
+// Column dots in registers (SK_DOTS_REG): the K dot terms of a lane's row (3 dots x VEC
+// columns) are summed over the warp's WR row slots with a reduce-scatter -- at lane bit M
+// the lower lane keeps the lower half of the (zero-padded) values and the upper lane the
+// upper half, each adding the partner's copy in the order (lower lane, upper lane) -- so
+// after log2(WR) steps every lane holds ceil(K/WR)-ish values of ONE slice of the index
+// space (`base`, `valid` of them real), to accumulate across the sweep in registers.
+// Replaces 3*VEC shared-memory read-modify-writes per lane and row by ~K shuffles per pass.
+#ifndef SK_DOTS_REG
+#define SK_DOTS_REG 1
+#endif
+// Shapes where the register accumulators measured faster than the shared-memory slots
+// (B200, tools/ab_dots.sh, gpurun_out r2j): double w = 4 (400^3 with three dots 1.90 ->
+// 1.70 ms) and w = 32 (256^3 KPM step 5.3 -> 4.0 ms).  Elsewhere the slots win (w = 1,
+// 8, 16 and complex: the epilogue's extra live registers spill at 3 CTAs/SM; C3 C64
+// 5.0 vs 6.2 ms).
+template <class T, int W>
+constexpr bool dots_in_registers() {
+    return SK_DOTS_REG != 0 && (SK_DOTS_REG == 2 || (std::is_same_v<T, double> && (W == 4 || W == 32)));
+}
+template <int K, int M, int TPR>
+constexpr int rs_final() {
+    if constexpr (M >= TPR && M > 0) return rs_final<(K + 1) / 2, M / 2, TPR>();
+    else return K;
+}
+
+// the slice (first index, real count) a lane ends up with, without the data
+template <int K, int M, int TPR>
+__device__ __forceinline__ void rs_slice(int lane, int& base, int& valid) {
+    if constexpr (M >= TPR && M > 0) {
+        constexpr int H = (K + 1) / 2;
+        if (lane & M) {
+            base += H;
+            valid = valid > H ? valid - H : 0;
+        } else {
+            valid = valid < H ? valid : H;
+        }
+        rs_slice<H, M / 2, TPR>(lane, base, valid);
+    }
+}
+
+template <class T, int K, int M, int TPR>
+__device__ __forceinline__ void rs_step(T* v, int lane) {
+    if constexpr (M >= TPR && M > 0) {
+        using O = Ops<T>;
+        constexpr int H = (K + 1) / 2;
+        const bool up = (lane & M) != 0;
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+            const T lo = v[i];
+            const T hi = (H + i < K) ? v[H + i] : O::zero();
+            const T recv = shfl_xor(up ? lo : hi, M);
+            v[i] = up ? O::add(recv, hi) : O::add(lo, recv);
+        }
+        rs_step<T, H, M / 2, TPR>(v, lane);
+    }
+}
+
 // Remainder handling of the row-contiguous kernel: 0 = exact-size batch when the
 // row length is warp-uniform, 1 = predicated batch, 2 = predicated loads too.
 #ifndef SK_BATCH_UNROLL1
@@ -826,7 +883,8 @@ constexpr std::size_t rows_stage_bytes() {
 }
 template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
-    return rows_stage_bytes<T, W, DOTS>() + (DOTS ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) +
+    return rows_stage_bytes<T, W, DOTS>() +
+           (DOTS && !dots_in_registers<T, W>() ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) +
            128;
 }
 
@@ -956,7 +1014,16 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
         T* dacc = reinterpret_cast<T*>(smem + rows_stage_bytes<T, W, DOTS>());
         const int cl = warp * 32 + lane;  // consumer lane
         constexpr int NCL = kNCW * 32;
-        if constexpr (DOTS) {
+        constexpr bool kDR = dots_in_registers<T, W>();
+        constexpr int KD = 3 * VEC;                       // dot terms per lane and row
+        constexpr int KF = rs_final<KD, 16, TPR>();        // register accumulators per lane
+        T dreg[kDR && DOTS ? KF : 1];
+        int dbase = 0, dvalid = KD;                        // slice of the KD terms this lane keeps
+        if constexpr (DOTS && kDR) rs_slice<KD, 16, TPR>(lane, dbase, dvalid);
+        if constexpr (DOTS && kDR) {
+#pragma unroll
+            for (int q = 0; q < KF; ++q) dreg[q] = O::zero();
+        } else if constexpr (DOTS) {
 #pragma unroll
             for (int q = 0; q < 3 * VEC; ++q) dacc[q * NCL + cl] = O::zero();
         }
@@ -1103,6 +1170,11 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             }
             // fused epilogue (spmv_epilogue.hpp:12-36); a remote-part sweep writes the
             // local rows its stored rows map to (row_map)
+            T dt[kDR && DOTS ? KD : 1];
+            if constexpr (kDR && DOTS) {
+#pragma unroll
+                for (int q = 0; q < KD; ++q) dt[q] = O::zero();
+            }
             if (row < row_end) {
                 const gidx orow = MAPPED ? gidx(__ldg(a.row_map + row)) : gidx(row);
                 const bool fin = !deferred(a.defer_mask, orow);
@@ -1135,7 +1207,14 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                         else
                             st_vec<T, VEC>(zp, zv);
                     }
-                    if constexpr (DOTS) {
+                    if constexpr (DOTS && kDR) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            if (a.flags & kFlagDotYY) dt[e] = O::mul(O::conj(out.v[e]), out.v[e]);
+                            if (a.flags & kFlagDotXY) dt[VEC + e] = O::mul(O::conj(xs.v[e]), out.v[e]);
+                            if (a.flags & kFlagDotXX) dt[2 * VEC + e] = O::mul(O::conj(xs.v[e]), xs.v[e]);
+                        }
+                    } else if constexpr (DOTS) {
 #pragma unroll
                         for (int e = 0; e < VEC; ++e) {
                             T* dp = dacc + e * NCL + cl;
@@ -1146,11 +1225,26 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                     }
                 }
             }
+            if constexpr (DOTS && kDR) {
+                // warp-uniform: sum the pass's rows slot-wise, keep this lane's slice
+                rs_step<T, KD, 16, TPR>(dt, lane);
+#pragma unroll
+                for (int q = 0; q < KF; ++q) dreg[q] = O::add(dreg[q], dt[q]);
+            }
             }  // pass
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // matrix data of the tile consumed
         }
-        if constexpr (DOTS) {
+        if constexpr (DOTS && kDR) {
+            // every (dot, column) lives in exactly one lane of the warp: its warp total
+#pragma unroll
+            for (int q = 0; q < KF; ++q) {
+                if (q < dvalid) {
+                    const int idx = dbase + q;  // dot * VEC + e
+                    red[warp][idx / VEC][sub * VEC + idx % VEC] = dreg[q];
+                }
+            }
+        } else if constexpr (DOTS) {
             // lanes of a row slot -> warp total per column (fixed butterfly order)
 #pragma unroll
             for (int q = 0; q < 3; ++q) {

@@ -155,6 +155,7 @@ _EXT = [
                                      C.POINTER(gidx), C.POINTER(C.c_int)]),
     ("sellkit_ext_mat_export", err_t, [vp, vp, vp, vp, vp, vp, vp, vp]),
     ("sellkit_ext_mat_set_sweep_order", err_t, [vp, lidx, vp, gidx]),
+    ("sellkit_ext_mat_set_apply_override", err_t, [vp, vp, vp]),
     ("sellkit_ext_densemat_storage", err_t, [vp, C.POINTER(vp), C.POINTER(lidx), C.POINTER(C.c_int),
                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("sellkit_ext_densemat_fill_hash", err_t, [vp, C.c_uint64]),

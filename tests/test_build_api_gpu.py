@@ -128,3 +128,31 @@ def test_capi_identity_callback_and_empty_rows(sk, tmp_path):
     h = vp()
     sk.call("sellkit_mat_to_crs", G, C.byref(h))
     assert _gcrs(sellkit.Crs(sk, h, sellkit.R64), tmp_path / "g.gcrs") == _gcrs(gaps, tmp_path / "g0.gcrs")
+
+
+def test_apply_override_matrix_free(sk):
+    """sellkit_ext_mat_set_apply_override: the matrix-free operator slot of the reference
+    (SellMatrix::apply_override, sellcs.hpp:116-119), KAT of unit_sparse.cpp:520-531:
+    an override computing y = 2 x on identity(3) gives y[1] = 4; validation still runs
+    first; removing the override restores the built-in multiply."""
+    import ctypes as C
+    A = sk.crs([0, 1, 2, 3], [0, 1, 2], np.ones(3)).build(1, 1)
+    calls = []
+    CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+    def fn(y, x, opts, stream, ctx):
+        calls.append(stream)
+        two, zero = np.array([2.0]), np.array([0.0])
+        return sk.lib.sellkit_axpby(y, x, two.ctypes.data, zero.ctypes.data)  # y = 2 x
+    cb = CB(fn)
+    sk.call("sellkit_ext_mat_set_apply_override", A.h, cb, None)
+    x = sk.densemat_from(np.array([[1.0], [2.0], [3.0]]))
+    y = sk.densemat_from(np.zeros((3, 1)))
+    sk.spmv(y, A, x)
+    assert y.copy_out()[1, 0] == 4.0 and len(calls) == 1 and calls[0]
+    with pytest.raises(sellkit.SellkitError) as e:          # validated before the override runs
+        sk.spmv(sk.densemat(4, 1), A, x)
+    assert e.value.code == sellkit.ERR_SHAPE and len(calls) == 1
+    sk.call("sellkit_ext_mat_set_apply_override", A.h, None, None)
+    sk.spmv(y, A, x)
+    assert y.copy_out()[:, 0].tolist() == [1.0, 2.0, 3.0]

@@ -17,6 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_functions(header):
     text = open(os.path.join(ROOT, "include", header)).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"\btypedef\b[^;]*;", "", text, flags=re.S)  # function-pointer types are not functions
     names = set(re.findall(r"\b(sellkit_\w+)\s*\(", text))
     # typedef'd function pointer names are not functions
     return sorted(n for n in names if n not in {"sellkit_row_fn", "sellkit_task_fn"})

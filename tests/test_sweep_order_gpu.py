@@ -55,3 +55,32 @@ def test_sweep_order_checks(sk):
     A.set_sweep_order(256, None)
     sk.spmv(y2, A, x)
     assert np.array_equal(y1.copy_out(), y2.copy_out())
+
+
+@pytest.mark.parametrize("dt,w", [(sellkit.C64, 16), (sellkit.R64, 8)])
+def test_auto_locality_order(sk, dt, w, monkeypatch):
+    """The automatic locality order (default policy) engages when the coupling distance
+    times the streamed bytes per row exceeds half the L2 (here a 1 MB L2 is assumed via
+    SELLKIT_AUTO_ORDER_L2): y bit-identical to the natural order, dots within tolerance."""
+    lx, ly, lz = 64, 16, 16
+    N = 4 * lx * ly * lz
+    npdt = sellkit.NP_DTYPE[dt]
+    xv = hash_block(N, w, 42).astype(npdt)
+    y0 = hash_block(N, w, 43).astype(npdt)
+    flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX
+
+    def run(A):
+        x, y = sk.densemat_from(xv), sk.densemat_from(y0)
+        d = np.zeros(3 * w, npdt)
+        sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, dot=d)
+        return y.copy_out(), d
+    A = sk.crs_ti(lx, ly, lz, 1.0, dt=dt).build(32, 256)
+    A.set_sweep_order(256, None)                      # natural row order
+    yn, dn = run(A)
+    monkeypatch.setenv("SELLKIT_AUTO_ORDER_L2", "1000000")
+    B = sk.crs_ti(lx, ly, lz, 1.0, dt=dt).build(32, 256)   # default policy: automatic
+    ya, da = run(B)
+    assert np.array_equal(yn, ya)
+    scale = np.concatenate([np.sum(np.abs(yn) ** 2, 0), np.sum(np.abs(xv) * np.abs(yn), 0),
+                            np.sum(np.abs(xv) ** 2, 0)])
+    assert np.all(np.abs(dn - da) <= 1e-12 * (1 + scale))
