@@ -99,6 +99,16 @@ sellkit_error sellkit_ext_densemat_storage(const sellkit_densemat* m, void** dat
  * Row index i is the storage row. */
 sellkit_error sellkit_ext_densemat_fill_hash(sellkit_densemat* m, uint64_t seed);
 
+/* Timeline of the single-process distributed SpMV (sellkit_dist_spmv / _nocomm): with
+ * trace on, each call records per rank 5 times in ms after the call's start --
+ * exchange start and end (the rank's communication stream: packing its send lists into
+ * the receivers' halo blocks), local-sweep start and end, remote-sweep end (the main
+ * stream) -- and synchronises.  sellkit_ext_ctx_timeline copies min(*nvalues, 5 k)
+ * values (rank-major) and sets *nvalues = 5 k; -1 marks an event not recorded (no
+ * exchange, or a rank on another device than rank 0). */
+sellkit_error sellkit_ext_ctx_set_trace(sellkit_ctx* ctx, int on);
+sellkit_error sellkit_ext_ctx_timeline(const sellkit_ctx* ctx, double* out, int* nvalues);
+
 /* ------------------------------------------ one process per GPU (NCCL) --
  * The multi-process counterpart of sellkit_ctx (which drives all ranks from one
  * process).  Each process owns rank `rank` of a BY_ROWS / BY_NNZ partition

@@ -251,12 +251,45 @@ void densemat_copy(DenseMat& dst, const DenseMat& src_in) {
     auto& rt = runtime(dev);
     if (dst.mem == MemKind::device && src.mem == MemKind::device) {
         if (dst.device != src.device) {
-            // cross-device: bring src over as a compact row-major temp
-            DeviceGuard gs(src.device);
-            std::vector<unsigned char> host(std::size_t(src.nrows) * src.ncols * es);
-            densemat_copy_out(src, host.data(), std::size_t(src.nrows) * src.ncols);
-            DeviceGuard gd(dst.device);
-            densemat_copy_in(dst, host.data(), std::size_t(src.nrows) * src.ncols);
+            // cross-device: one peer copy (NVLink / PCIe P2P, no host bounce) of a compact
+            // row-major image of src, then the layout copy on the destination device
+            const std::size_t n = std::size_t(src.nrows) * src.ncols;
+            auto& rs = runtime(src.device);
+            DeviceBuffer src_tmp;
+            const void* image = src.data;
+            if (!contiguous_row_major(src)) {
+                DeviceGuard gs(src.device);
+                src_tmp = DeviceBuffer(std::max<std::size_t>(n * es, 16), src.device);
+                DenseMat t = densemat_view_plain(src.dt, src_tmp.get(), n, src.nrows, src.ncols, src.ncols,
+                                                 Order::row_major);
+                densemat_copy(t, src);
+                image = src_tmp.get();
+            }
+            cudaEvent_t ready;
+            {
+                DeviceGuard gs(src.device);
+                CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+                CK(cudaEventRecord(ready, rs.stream));
+            }
+            CK(cudaStreamWaitEvent(rt.stream, ready, 0));
+            if (contiguous_row_major(dst)) {
+                CK(cudaMemcpyPeerAsync(dst.data, dst.device, image, src.device, n * es, rt.stream));
+            } else {
+                DeviceBuffer dst_tmp(std::max<std::size_t>(n * es, 16), dst.device);
+                CK(cudaMemcpyPeerAsync(dst_tmp.get(), dst.device, image, src.device, n * es, rt.stream));
+                DenseMat t = densemat_view_plain(dst.dt, dst_tmp.get(), n, dst.nrows, dst.ncols, dst.ncols,
+                                                 Order::row_major);
+                DAcc d = dacc(dst), s2 = dacc(t);
+                visit_dt(dst.dt, [&]<class T>() {
+                    copy_kernel<T><<<grid_for(gidx(dst.nrows) * dst.ncols, 256, rt), 256, 0, rt.stream>>>(
+                        d, s2, dst.nrows, dst.ncols);
+                    return 0;
+                });
+                CK(cudaGetLastError());
+                CK(cudaStreamSynchronize(rt.stream));  // before dst_tmp is freed
+            }
+            CK(cudaStreamSynchronize(rt.stream));      // before src_tmp / the event go
+            CK(cudaEventDestroy(ready));
             return;
         }
         DAcc d = dacc(dst), s = dacc(src);

@@ -281,7 +281,10 @@ void rank_build_device(RankPart& part, lidx C, lidx sigma) {
                            rt.stream));
     }
     if (!part.comm) {
-        CK(cudaStreamCreateWithFlags(&part.comm, cudaStreamNonBlocking));
+        // highest priority: the small pack kernels get SMs ahead of the persistent local sweep
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&part.comm, cudaStreamNonBlocking, hi));
         CK(cudaEventCreateWithFlags(&part.ev_x, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&part.ev_halo, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&part.ev_done, cudaEventDisableTiming));
@@ -522,6 +525,22 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
     const lidx w = x.width;
     const std::size_t es = value_bytes(ctx.dt);
     for (int r = 0; r < k; ++r) ensure_scratch(ctx.scratch[r], *ctx.ranks[r], w);
+    // optional timeline (sellkit_ext_ctx_set_trace): per rank, timing events at the
+    // exchange start / end (comm stream) and the local-sweep start / end and remote-sweep
+    // end (main stream), relative to one start event on rank 0's device
+    const bool trace = ctx.trace;
+    auto tev = [&](int r, int i) -> cudaEvent_t { return ctx.tev[std::size_t(r) * kTraceEvents + i + 1]; };
+    if (trace) {
+        if (ctx.tev.empty()) {
+            ctx.tev.resize(std::size_t(k) * kTraceEvents + 1);
+            for (std::size_t i = 0; i < ctx.tev.size(); ++i) {
+                DeviceGuard g(ctx.ranks[i == 0 ? 0 : (i - 1) / kTraceEvents]->device);
+                CK(cudaEventCreate(&ctx.tev[i]));
+            }
+        }
+        DeviceGuard g(ctx.ranks[0]->device);
+        CK(cudaEventRecord(ctx.tev[0], runtime(ctx.ranks[0]->device).stream));
+    }
 
     // 1. halo exchange: each owner packs straight into the requester's halo block
     if (!nocomm) {
@@ -531,6 +550,7 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
             auto& rt = runtime(part.device);
             CK(cudaEventRecord(part.ev_x, rt.stream));
             CK(cudaStreamWaitEvent(part.comm, part.ev_x, 0));
+            if (trace) CK(cudaEventRecord(tev(r, 0), part.comm));
             for (std::size_t s = 0; s < part.plan.send_to.size(); ++s) {
                 const int to = part.plan.send_to[s];
                 RankPart& dst = *ctx.ranks[to];
@@ -560,6 +580,7 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
                     ctx.msgs += 1;
                 }
             }
+            if (trace) CK(cudaEventRecord(tev(r, 1), part.comm));
             CK(cudaEventRecord(part.ev_halo, part.comm));
         }
     }
@@ -572,12 +593,35 @@ void dist_spmv(DistVec& y, DistContext& ctx, const DistVec& x, const SpmvOptions
             for (int owner : part.plan.recv_owner) CK(cudaStreamWaitEvent(rt.stream, ctx.ranks[owner]->ev_halo, 0));
         }
         DenseMat* zr = chain ? &z->parts[r] : nullptr;
+        if (trace) CK(cudaEventRecord(tev(r, 2), rt.stream));
+        bool local_marked = false;
         rank_sweeps(part, ctx.scratch[r], const_cast<DenseMat&>(y.parts[r]), x.parts[r], o, zr, nocomm, rt.stream,
                     [&] {
+                        if (trace) CK(cudaEventRecord(tev(r, 3), rt.stream));
+                        local_marked = true;
                         for (int owner : part.plan.recv_owner)
                             CK(cudaStreamWaitEvent(rt.stream, ctx.ranks[owner]->ev_halo, 0));
                     });
+        if (trace && !local_marked) CK(cudaEventRecord(tev(r, 3), rt.stream));
+        if (trace) CK(cudaEventRecord(tev(r, 4), rt.stream));
         CK(cudaEventRecord(part.ev_done, rt.stream));
+    }
+    if (trace) {
+        ctx.timeline.assign(std::size_t(k) * kTraceEvents, -1.0);
+        for (int r = 0; r < k; ++r) {
+            DeviceGuard g(ctx.ranks[r]->device);
+            CK(cudaDeviceSynchronize());
+        }
+        for (int r = 0; r < k; ++r) {
+            if (ctx.ranks[r]->device != ctx.ranks[0]->device) continue;  // one clock per device
+            for (int i = 0; i < kTraceEvents; ++i) {
+                if (nocomm && i < 2) continue;
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, ctx.tev[0], tev(r, i)) == cudaSuccess)
+                    ctx.timeline[std::size_t(r) * kTraceEvents + i] = ms;
+                cudaGetLastError();
+            }
+        }
     }
     // 3. dots: per-rank partials summed in rank order on rank 0's device
     //    (partition.hpp:379-394), one copy of the requested thirds to the caller
@@ -1314,6 +1358,22 @@ sellkit_error sellkit_ctx_reset_comm_stats(sellkit_ctx* ctx) {
 }
 
 void sellkit_ctx_destroy(sellkit_ctx* ctx) { delete ctx; }
+
+sellkit_error sellkit_ext_ctx_set_trace(sellkit_ctx* ctx, int on) {
+    return sk::guarded([&] {
+        sk::require(ctx != nullptr, "null handle");
+        ctx->p->trace = on != 0;
+    });
+}
+
+sellkit_error sellkit_ext_ctx_timeline(const sellkit_ctx* ctx, double* out, int* nvalues) {
+    return sk::guarded([&] {
+        sk::require(ctx && nvalues, "null argument");
+        const auto& t = ctx->p->timeline;
+        if (out) std::copy(t.begin(), t.begin() + std::min<std::size_t>(t.size(), std::size_t(*nvalues)), out);
+        *nvalues = int(t.size());
+    });
+}
 
 sellkit_error sellkit_dvec_create(const sellkit_ctx* ctx, sellkit_lidx width, sellkit_order order, sellkit_dvec** out) {
     return sk::guarded([&] {

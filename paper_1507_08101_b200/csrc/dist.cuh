@@ -90,6 +90,8 @@ struct RankScratch {
     DeviceBuffer dots;     // 3 * width
 };
 
+constexpr int kTraceEvents = 5;  // exchange start/end, local start/end, remote end
+
 struct DistContext {
     Datatype dt = Datatype::r64;
     gidx n = 0, nnz = 0;
@@ -100,6 +102,14 @@ struct DistContext {
     bool record = false;
     std::uint64_t bytes = 0, msgs = 0;
     DeviceBuffer dots_all;      // k x 3w dot partials on rank 0's device
+    bool trace = false;         // record a per-rank timeline of each dist_spmv
+    std::vector<cudaEvent_t> tev;
+    std::vector<double> timeline;  // k x kTraceEvents, ms after the call's start (-1: none)
+    ~DistContext() {
+        for (auto e : tev) cudaEventDestroy(e);
+    }
+    DistContext() = default;
+    DistContext(const DistContext&) = delete;
     int ndev = 1;
     std::vector<char> peer_ok;  // [ndev x ndev]: peer access enabled from i to j
     // may rank memory on `dst` be written by kernels running on `src`?

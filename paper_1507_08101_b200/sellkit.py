@@ -159,6 +159,8 @@ _EXT = [
     ("sellkit_ext_densemat_storage", err_t, [vp, C.POINTER(vp), C.POINTER(lidx), C.POINTER(C.c_int),
                                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("sellkit_ext_densemat_fill_hash", err_t, [vp, C.c_uint64]),
+    ("sellkit_ext_ctx_set_trace", err_t, [vp, C.c_int]),
+    ("sellkit_ext_ctx_timeline", err_t, [vp, vp, C.POINTER(C.c_int)]),
     ("sellkit_ext_nccl_unique_id", err_t, [vp]),
     ("sellkit_ext_rankctx_create", err_t, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     ("sellkit_ext_rankctx_recv_count", err_t, [vp, C.POINTER(C.c_int)]),

@@ -154,3 +154,24 @@ def test_rank_context_world1(sk, orc):
     yo, _, do = orc.spmv(Ao, xs, flags=sellkit.DOT_YY)
     assert np.array_equal(y.copy_out(), yo)
     assert abs(dots[0] - do[0]) <= 1e-12 * (1 + abs(do[0]))
+
+
+def test_dist_timeline_trace(sk):
+    """sellkit_ext_ctx_set_trace / _timeline: per rank exchange and sweep intervals of
+    one dist_spmv, ordered as the streams run them."""
+    import ctypes as C
+    n, k, w = 24, 3, 4
+    ctx = dist.DistContext(sk, sk.crs_stencil(7, n), k, 32, 256, record=False)
+    x, y = ctx.vec(w), ctx.vec(w)
+    sk.call("sellkit_ext_ctx_set_trace", ctx.h, 1)
+    ctx.spmv(y, x)
+    cnt = C.c_int(0)
+    sk.call("sellkit_ext_ctx_timeline", ctx.h, None, C.byref(cnt))
+    assert cnt.value == 5 * k
+    buf = (C.c_double * cnt.value)()
+    sk.call("sellkit_ext_ctx_timeline", ctx.h, buf, C.byref(cnt))
+    t = np.array(buf[:]).reshape(k, 5)
+    for r in range(k):
+        xs, xe, ls, le, re_ = t[r]
+        assert 0 <= xs <= xe and 0 <= ls <= le <= re_, t[r]
+        assert xe <= re_  # the remote sweep waited for the halo
