@@ -174,4 +174,7 @@ def test_dist_timeline_trace(sk):
     for r in range(k):
         xs, xe, ls, le, re_ = t[r]
         assert 0 <= xs <= xe and 0 <= ls <= le <= re_, t[r]
-        assert xe <= re_  # the remote sweep waited for the halo
+        # the remote sweep waited for the halo of its owners (the neighbouring slabs)
+        for o in (r - 1, r + 1):
+            if 0 <= o < k:
+                assert t[o][1] <= re_, (r, o, t)
