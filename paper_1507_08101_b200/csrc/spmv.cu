@@ -111,8 +111,14 @@ static const int* auto_sweep_order(const SellMat& A, lidx w, std::uint32_t flags
     const double vec = es * w;
     const double row_bytes = vec + nnz_row * (es + 4.0) + vec * (1.0 + ((flags & kFlagAxpby) ? 1.0 : 0.0) +
                                                                  ((flags & kFlagChain) ? 2.0 : 0.0));
+    // 64-byte RHS rows (double w = 8) stream more matrix than x per row: there the slab
+    // orders measured slower at every slab size (400^3: 2.38 -> 2.56-2.63 ms; 320^3:
+    // 1.08 -> 1.21-1.35 ms), so they keep the row order
+    if (vec < 128.0) return nullptr;
     const char* e_l2 = std::getenv("SELLKIT_AUTO_ORDER_L2");  // cache size the decision assumes (tests)
-    const double l2 = e_l2 ? std::atof(e_l2) : double(rt.l2_bytes);
+    // what the sweep can count on keeping: about half the L2 (measured best over
+    // 1/8 ... 1 L2 on C2 w = 16/32, 320^3 / 400^3 w = 16 and C3 C64/R64, profiles r2s)
+    const double l2 = 0.476 * (e_l2 ? std::atof(e_l2) : double(rt.l2_bytes));
     if (double(D) * row_bytes <= 0.5 * l2) return nullptr;  // the reuse window already fits L2
     constexpr int kBlockRgs = 8;                              // 256-row blocks
     const gidx brows = 32 * kBlockRgs;

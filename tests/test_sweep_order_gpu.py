@@ -57,7 +57,7 @@ def test_sweep_order_checks(sk):
     assert np.array_equal(y1.copy_out(), y2.copy_out())
 
 
-@pytest.mark.parametrize("dt,w", [(sellkit.C64, 16), (sellkit.R64, 8)])
+@pytest.mark.parametrize("dt,w", [(sellkit.C64, 16), (sellkit.R64, 16), (sellkit.R64, 32)])
 def test_auto_locality_order(sk, dt, w, monkeypatch):
     """The automatic locality order (default policy) engages when the coupling distance
     times the streamed bytes per row exceeds half the L2 (here a 1 MB L2 is assumed via
