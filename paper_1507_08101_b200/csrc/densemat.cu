@@ -220,13 +220,22 @@ DenseMat densemat_view(const DenseMat& p, lidx row_begin, lidx row_end, const li
     return v;
 }
 
-Staged::Staged(DenseMat& m, bool load) : orig(&m) {
+Staged::Staged(DenseMat& m, bool load, int slot) : orig(&m) {
     if (m.mem == MemKind::device) {
         dev = m;
         return;
     }
     staged = true;
-    dev = densemat_create(m.dt, m.nrows, m.ncols, m.order);
+    if (slot >= 0) {
+        auto& rt = runtime(current_device());
+        const std::size_t n = std::size_t(m.nrows) * m.ncols;
+        void* buf = rt.stage_bytes(slot, std::max<std::size_t>(n * m.esize(), 256));
+        dev = m.order == Order::row_major
+                  ? densemat_view_plain(m.dt, buf, n, m.nrows, m.ncols, m.ncols, Order::row_major)
+                  : densemat_view_plain(m.dt, buf, n, m.nrows, m.ncols, m.nrows, Order::col_major);
+    } else {
+        dev = densemat_create(m.dt, m.nrows, m.ncols, m.order);
+    }
     if (load) densemat_copy(dev, m);
 }
 

@@ -142,7 +142,9 @@ struct Staged {
     DenseMat* orig = nullptr;
     DenseMat dev;
     bool staged = false;
-    Staged(DenseMat& m, bool load);
+    // slot >= 0: stage into the device runtime's reusable staging buffer `slot` (0..2)
+    // instead of a fresh allocation per call (host-resident spmv operands)
+    Staged(DenseMat& m, bool load, int slot = -1);
     void write_back();
 };
 

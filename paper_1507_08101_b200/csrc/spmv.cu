@@ -470,13 +470,14 @@ void spmv(DenseMat& y, const SellMat& A, const DenseMat& x_in, const SpmvOptions
     DeviceGuard g(A.device);
     auto& rt = runtime(A.device);
     if (x.mem == MemKind::host && y.mem == MemKind::host && spmv_host_streamed(y, A, x, o)) return;
-    Staged xs(x, true);
-    Staged ys(y, (f & kFlagAxpby) != 0);
+    // host operands go through the runtime's reusable staging buffers (slots 0..2)
+    Staged xs(x, true, 0);
+    Staged ys(y, (f & kFlagAxpby) != 0, 1);
     DenseMat zdummy;
     std::unique_ptr<Staged> zs;
     SpmvOptions run = o;
     if (f & kFlagChain) {
-        zs = std::make_unique<Staged>(*o.z, true);
+        zs = std::make_unique<Staged>(*o.z, true, 2);
         run.z = &zs->dev;
     } else {
         run.z = nullptr;

@@ -8,8 +8,8 @@ through stream memory operations, never inside a kernel.
 
 For each golden case of tests/golden/dist.npz with k == WORLD_SIZE, this rank
 builds its row block from the golden CRS (global columns), connects, and runs
-the plain sweep (three dots) and the fused cases f1/f2 three times each (eager,
-graph capture, graph replay), writing its rows of y / z (original order) and
+the plain sweep (three dots) and the fused cases f1/f2 four times each (eager,
+graph capture, graph replay, eager with SMs reserved for the halo pack), writing its rows of y / z (original order) and
 the dots to <outdir>/rank<r>.npz for the parent test to compare.
 """
 import ctypes as C
@@ -82,7 +82,9 @@ def main():
                 else:
                     o.gamma = sc(gam[0])
             o.dot = C.c_void_p(dots_dev.data_ptr())
-            for rep in range(3):  # eager, capture + replay, replay
+            for rep in range(4):  # eager, capture + replay, replay, eager with SMs left to the pack
+                if rep == 3:
+                    rc.set_options(graphs=0, reserve_sms=16)
                 if y0 is not None:
                     yd.copy_in(stored(y0))
                     zd.copy_in(stored(z0))
@@ -95,6 +97,7 @@ def main():
                 out[f"{key}|{fname}|{rep}|y"] = ys[perm]
                 out[f"{key}|{fname}|{rep}|z"] = zs[perm]
                 out[f"{key}|{fname}|{rep}|dot"] = dots_dev.cpu().numpy()
+            rc.set_options(graphs=1, reserve_sms=0)
         out[f"{key}|stats"] = np.array([rc.stats()["bytes"], rc.stats()["msgs"]], np.int64)
         rc.close()
         tdist.barrier()

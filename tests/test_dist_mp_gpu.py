@@ -5,8 +5,8 @@ of the reference's golden matrices (tests/golden/dist.npz), connect through the
 library's CUDA-IPC transport (send slots pulled by copy-engine peer copies,
 stream-ordered flags -- no kernel waits on another rank, so ranks sharing one
 GPU cannot deadlock), and run y = A x with three dots plus the fused golden
-cases f1/f2 (shift/vshift, AXPBY, chain, dots) three times each: eager, CUDA
-graph capture, graph replay.  Every repetition must reproduce the reference's
+cases f1/f2 (shift/vshift, AXPBY, chain, dots) four times each: eager, CUDA
+graph capture, graph replay, eager with SMs reserved for the pack.  Every repetition must reproduce the reference's
 own dist_spmv (proj/src/partition.hpp:423-549) bit for bit in y and z, and its
 dots within 1e-12 * (1 + sum |x||y|) (the reference sums its dots per worker).
 """
@@ -76,7 +76,7 @@ def test_multiprocess_matches_reference_golden(golden, k, transport):
         n = int(off[-1])
         runs = [("plain", key, g[key + "|x"])] + [(f, f"{key}|{f}", g[f"{key}|{f}|x"]) for f, _, _ in FUSED]
         for fname, gk, xv in runs:
-            for rep in range(3):
+            for rep in range(4):
                 y = np.concatenate([res[r][f"{key}|{fname}|{rep}|y"] for r in range(k)])
                 dots = res[0][f"{key}|{fname}|{rep}|dot"]
                 assert y.shape == (n, w)
@@ -96,10 +96,12 @@ def test_multiprocess_matches_reference_golden(golden, k, transport):
                         if flags & (8 << s):  # DOT_YY << s
                             part = slice(s * w, (s + 1) * w)
                             assert np.all(np.abs(dots[part] - want[part]) <= 1e-12 * (1 + sc[part])), (key, fname)
-                # graph replays repeat the eager result bit for bit
-                assert np.array_equal(dots, res[0][f"{key}|{fname}|0|dot"])
-        # halo bytes: the reference's count (minus its dot allreduce) per step, 9 steps;
+                # graph replays repeat the eager result bit for bit (rep 3 runs a smaller
+                # sweep grid, so its dot partials -- not y or z -- may differ in the last bits)
+                if rep < 3:
+                    assert np.array_equal(dots, res[0][f"{key}|{fname}|0|dot"])
+        # halo bytes: the reference's count (minus its dot allreduce) per step, 12 steps;
         # the dot exchange adds 2(k-1) * 3w doubles per rank and step
         halo = int(g[key + "|comm"][0]) - 2 * (k - 1) * 3 * w * 8
         total = sum(int(res[r][f"{key}|stats"][0]) for r in range(k))
-        assert total == 9 * halo + 9 * k * 2 * (k - 1) * 3 * w * 8, key
+        assert total == 12 * halo + 12 * k * 2 * (k - 1) * 3 * w * 8, key
