@@ -339,7 +339,8 @@ KernelVariant select_kernel(lidx chunk_height, lidx block_width, Order order) {
 std::size_t spmv_scratch_bytes(Datatype dt, lidx width, int num_sms) {
     const std::size_t W = std::size_t(width);
     const std::size_t max_parts = std::size_t(num_sms) * 32 * ((W + kGW - 1) / kGW + 1);
-    return (W + 3 * W + max_parts * 3 * std::max<std::size_t>(W, kGW)) * value_bytes(dt) + 256;
+    // + 256 B of alignment slack + 256 B holding the dynamic-tile counter
+    return (W + 3 * W + max_parts * 3 * std::max<std::size_t>(W, kGW)) * value_bytes(dt) + 512;
 }
 
 void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOptions& o, const SpmvHooks& hooks) {
@@ -414,6 +415,7 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         T* gl = reinterpret_cast<T*>(sc);
         T* res = gl + W;
         a.partial = res + 3 * W;
+        a.tile_counter = reinterpret_cast<int*>(sc + need - 256);  // zeroed per launch when used
         if (o.flags & kFlagVshift) {
             CK(cudaMemcpyAsync(gl, o.gamma_list, W * es, cudaMemcpyDefault, st));
             a.gamma_list = gl;

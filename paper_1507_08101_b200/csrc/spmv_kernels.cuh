@@ -73,6 +73,8 @@ struct KArgs {
     int sweep_brg;           // 0 = natural order
     int grid_sms;            // launch: SMs the grid may fill (0 = all; the rest stay free for a
                              // concurrent halo pack on the communication stream)
+    int* tile_counter;       // rows kernels without dots: tiles handed out by an atomic counter
+                             // (zeroed before the launch) instead of a static round robin
 };
 
 namespace spmv_detail {
@@ -832,6 +834,10 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 // tile (fewer active warps) or, past a stage, read the matrix from global memory.
 // The sizes are compile-time: the same kernel with runtime stage sizes was
 // scheduled worse by ptxas (2.8 ms, products hoisted between the gathers).
+#ifndef SK_DYN_TILES
+#define SK_DYN_TILES 1
+#endif
+
 #ifndef SK_RMINB
 #define SK_RMINB 4
 #endif
@@ -929,14 +935,40 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
         return a.rg0 + t * rgt;
     };
 
+    // dynamic tiles (epilogue kernels without dots, whose results do not depend on which
+    // CTA sweeps a tile): the producer takes the next tile from a global counter, so
+    // the sweep front stays one contiguous band (x reuse) and no CTA trails at the end;
+    // a tile index >= ntiles in the stage header tells the consumers to stop
+    // (measured, tools/ab_plain.sh r2v: 400^3 w = 8 AXPBY 3.35 -> 2.71 ms; the plain
+    // epilogue-free kernels keep the static deal, 2.40 vs 2.47 ms, C1 22 vs 25 us)
+    constexpr bool kDynOK = SK_DYN_TILES && !DOTS && !PLAIN;
+    const bool dyn = kDynOK && a.tile_counter != nullptr;
     if (warp == kNCW) {
         // ------------------------------------------------- producer warp (as spmv_tma_kernel)
         const unsigned long long pol = l2_evict_first_policy();
+        auto grab = [&](int it) -> gidx {
+            if (!dyn) return tile_of(it, seg);
+            int v = 0;
+            if (lane == 0) v = atomicAdd(a.tile_counter, 1);
+            return gidx(__shfl_sync(0xffffffffu, v, 0));
+        };
+        gidx t_cur = grab(0);
         for (int it = 0;; ++it) {
-            const gidx t = tile_of(it, seg);
-            if (t >= ntiles) break;
+            const gidx t = t_cur;
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
+            if (t >= ntiles) {
+                if (dyn) {  // tell the consumers there is no further tile
+                    mbar_wait(&empty[s], (k & 1u) ^ 1u);
+                    if (lane == 0) {
+                        hdr[s].nchunks = -1;
+                        mbar_arrive(&full[s]);
+                    }
+                }
+                break;
+            }
+            const gidx t_next = grab(it + 1);
+            t_cur = t_next;
             // the epilogue's y (AXPBY) and z (CHAIN) rows of this tile: one bulk L2
             // prefetch each, a stage ahead of the consumers, so the epilogue reads
             // hit L2 instead of adding a dependent HBM round trip per tile
@@ -991,7 +1023,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 }
             }
             if constexpr (SK_HDR_PREFETCH > 0 && (PLAIN || DOTS)) {
-                const gidx tn = tile_of(it + SK_HDR_PREFETCH, seg);
+                const gidx tn = dyn ? t_next : tile_of(it + SK_HDR_PREFETCH, seg);
                 if (tn < ntiles) {
                     const gidx cn0 = min(tile_rg(tn) * (32 / C), cend);
                     const gidx cn1 = min(cend, cn0 + chunks_per_tile);
@@ -1038,12 +1070,15 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
         constexpr int kMaxPasses = DOTS ? 1 : (SK_RTILE_ROWS / (kNCW * WR) > 1 ? SK_RTILE_ROWS / (kNCW * WR) : 1);
         const int passes = min(kMaxPasses, (rows_per_tile + kNCW * WR - 1) / (kNCW * WR));
         for (int it = 0;; ++it) {
-            const int t = seg == 1 ? it * int(gridDim.x) + int(blockIdx.x) : int(tile_of(it, seg));
-            if (t >= nt) break;
+            if (!dyn) {
+                const int t = seg == 1 ? it * int(gridDim.x) + int(blockIdx.x) : int(tile_of(it, seg));
+                if (t >= nt) break;
+            }
             const int s = it % kStages;
             const std::uint32_t k = std::uint32_t(it / kStages);
             mbar_wait(&full[s], k & 1u);
             const StageHdr& h = hdr[s];
+            if (dyn && h.nchunks < 0) break;  // the producer ran out of tiles
             const int tile_row0 = h.row0;  // the producer resolved the sweep order
             // a tile may hold several warp-row passes (narrow warps, short rows): the
             // per-tile work (barrier, header, release) is shared by all of them
@@ -1463,7 +1498,10 @@ inline int rows_mode() {
 }
 
 template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false>
-LaunchShape launch_tma_rows(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream_t st) {
+LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cudaStream_t st) {
+    KArgs<T> a = a_in;
+    if (DOTS || PLAIN || !SK_DYN_TILES) a.tile_counter = nullptr;
+    if (a.tile_counter) CK(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st));
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
