@@ -418,6 +418,9 @@ def run_ours(args, rank, world, local_rank):
                         if job is None else "per rank: H2D x, sellkit_ext_rank_spmv, D2H y; consecutive steps "
                         "overlap the upload with the previous download")}
 
+    if job is not None:
+        torch.cuda.synchronize()
+        job.close()  # collective: no rank frees IPC slots / leaves NCCL while a peer still uses them
     if rank != 0:
         return
     cb = None

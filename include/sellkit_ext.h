@@ -157,6 +157,8 @@ sellkit_error sellkit_ext_rankctx_stats(const sellkit_rankctx* rc, uint64_t* byt
                                         sellkit_lidx* n_halo, uint64_t* boundary_rows, sellkit_gidx* local_nnz,
                                         sellkit_gidx* remote_nnz);
 sellkit_error sellkit_ext_rankctx_row_perm(const sellkit_rankctx* rc, sellkit_lidx* row_perm);
+/* Destroy only after EVERY rank has finished its last sellkit_ext_rank_spmv (e.g. after a
+ * barrier): the other ranks map this rank's IPC slots / share its NCCL communicator. */
 void sellkit_ext_rankctx_destroy(sellkit_rankctx* rc);
 
 /* Host-only planning of one rank (no GPU needed): the partition.hpp:136-220 split

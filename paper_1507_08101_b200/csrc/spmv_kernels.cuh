@@ -837,6 +837,9 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 #ifndef SK_DYN_TILES
 #define SK_DYN_TILES 1
 #endif
+#ifndef SK_DYN_DOTS  // experiment: dynamic tiles for the dots kernels (dots then depend on timing)
+#define SK_DYN_DOTS 0
+#endif
 
 #ifndef SK_RMINB
 #define SK_RMINB 4
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
     // a tile index >= ntiles in the stage header tells the consumers to stop
     // (measured, tools/ab_plain.sh r2v: 400^3 w = 8 AXPBY 3.35 -> 2.71 ms; the plain
     // epilogue-free kernels keep the static deal, 2.40 vs 2.47 ms, C1 22 vs 25 us)
-    constexpr bool kDynOK = SK_DYN_TILES && !DOTS && !PLAIN;
+    constexpr bool kDynOK = SK_DYN_TILES && (!DOTS || SK_DYN_DOTS) && !PLAIN;
     const bool dyn = kDynOK && a.tile_counter != nullptr;
     if (warp == kNCW) {
         // ------------------------------------------------- producer warp (as spmv_tma_kernel)
@@ -1500,7 +1503,7 @@ inline int rows_mode() {
 template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false>
 LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     KArgs<T> a = a_in;
-    if (DOTS || PLAIN || !SK_DYN_TILES) a.tile_counter = nullptr;
+    if ((DOTS && !SK_DYN_DOTS) || PLAIN || !SK_DYN_TILES) a.tile_counter = nullptr;
     if (a.tile_counter) CK(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st));
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED>;

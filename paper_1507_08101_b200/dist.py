@@ -268,14 +268,26 @@ class RankContext:
         self.sk.call("sellkit_ext_rank_spmv", y.h, self.h, x.h, C.byref(opts), z.h if z is not None else None,
                      1 if nocomm else 0)
 
-    def close(self):
+    def close(self, group=None):
+        """Collective when connected: every rank must have finished its last step before
+        any rank frees the buffers the others map (CUDA IPC) or leaves the NCCL
+        communicator, so the ranks synchronise their device and meet at a barrier first."""
         if self.h:
+            if self.world > 1 and self.transport != "none":
+                import torch
+                import torch.distributed as tdist
+                torch.cuda.synchronize()
+                if tdist.is_available() and tdist.is_initialized():
+                    tdist.barrier(group=group if group is not None else getattr(self, "group", None))
             self.sk.lib.sellkit_ext_rankctx_destroy(self.h)
             self.h = None
 
     def __del__(self):
+        # interpreter shutdown: no collective possible any more; just release
         try:
-            self.close()
+            if self.h:
+                self.sk.lib.sellkit_ext_rankctx_destroy(self.h)
+                self.h = None
         except Exception:
             pass
 
@@ -300,6 +312,7 @@ def setup_rank(sk: Sellkit, rows_crs, row_offsets, rank: int, world: int, chunk_
     handshake (requests, IPC blobs / NCCL id) goes through ``torch.distributed``."""
     import torch.distributed as tdist
     rc = RankContext(sk, rows_crs, row_offsets, rank, chunk_height, sigma)
+    rc.group = group
     if world > 1:
         incoming = exchange_requests(rc.requests(), rank, world, group)
         for to in sorted(incoming):
@@ -343,6 +356,12 @@ class BenchJob:
 
     def kernel_ms(self, per_step: List[float]) -> float:
         return float(np.mean(per_step))
+
+    def close(self):
+        """Collective: release the rank context after every rank finished (see RankContext.close)."""
+        for obj in self.keep:
+            if isinstance(obj, RankContext):
+                obj.close()
 
 
 def bench_setup(sk: Sellkit, n: int, w: int, chunk_height: int, sigma: int, rank: int, world: int,

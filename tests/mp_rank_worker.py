@@ -99,8 +99,7 @@ def main():
                 out[f"{key}|{fname}|{rep}|dot"] = dots_dev.cpu().numpy()
             rc.set_options(graphs=1, reserve_sms=0)
         out[f"{key}|stats"] = np.array([rc.stats()["bytes"], rc.stats()["msgs"]], np.int64)
-        rc.close()
-        tdist.barrier()
+        rc.close()  # collective: waits for every rank before freeing the exported slots
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), **out)
     tdist.barrier()
     tdist.destroy_process_group()
