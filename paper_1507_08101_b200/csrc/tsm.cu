@@ -273,12 +273,21 @@ __device__ __forceinline__ void store_row(T* p, const T (&r)[N]) {
 #ifndef SK_TT_UR_MAX
 #define SK_TT_UR_MAX 8
 #endif
+#ifndef SK_TT_CHUNK_UR  // 32-byte chunks in flight per thread in the chunked TSMTTSM path
+#define SK_TT_CHUNK_UR 2
+#endif
+#ifndef SK_TSM_CHUNK    // 1: chunked paths for the 8- and 16-byte-row shapes (1x1, 2x2)
+#define SK_TSM_CHUNK 1
+#endif
 
 // TSMTTSM, m <= MM, k <= KK (MM, KK in {1,2,4,8}): each thread keeps the whole
 // m x k block in registers and walks its rows of the CTA's contiguous range;
 // warp butterfly + ordered CTA sum -> one partial per CTA (deterministic).
 // Compact operands with m == MM, k == KK load whole rows with vector accesses.
-template <class T, int MM, int KK, bool KAHAN>
+// R > 1 (compact m == MM, k == KK, MM * R * sizeof(T) == 32): a thread loads R consecutive
+// rows of V and of W with one 32-byte access each (1 x 1: four rows per LDG.256), UR2
+// chunks in flight -- the 8- and 16-byte rows otherwise leave too few bytes in flight.
+template <class T, int MM, int KK, bool KAHAN, int R = 1>
 __global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v, gidx vs, const T* __restrict__ w,
                                                          gidx ws, gidx n, int m, int k, gidx rows_per_cta, T* partial,
                                                          T* pcomp) {
@@ -324,6 +333,49 @@ __global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v
     constexpr int UR0 = !KAHAN && kUnroll ? 4 : 1;
     constexpr int UR = UR0 < SK_TT_UR_MAX ? UR0 : SK_TT_UR_MAX;
     gidx i = r0 + threadIdx.x;
+    if constexpr (R > 1) {
+        // chunks of R rows (the CTA range starts on a chunk; only the last CTA's end may not)
+        constexpr int UR2 = SK_TT_CHUNK_UR;
+        i = r0 + gidx(threadIdx.x) * R;
+        for (; i + gidx(UR2 - 1) * kT * R + R <= r1; i += gidx(UR2) * kT * R) {
+            T vr[UR2][R * MM], wr[UR2][R * KK];
+#pragma unroll
+            for (int u = 0; u < UR2; ++u) {
+                load_row<T, R * MM>(v + (i + gidx(u) * kT * R) * MM, vr[u]);
+                load_row<T, R * KK>(w + (i + gidx(u) * kT * R) * KK, wr[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < UR2; ++u)
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int a = 0; a < MM; ++a)
+#pragma unroll
+                        for (int b = 0; b < KK; ++b)
+                            acc[a][b] = O::fma(O::conj(vr[u][r * MM + a]), wr[u][r * KK + b], acc[a][b]);
+        }
+        for (; i < r1; i += gidx(kT) * R) {  // remaining chunks one at a time, the last one by rows
+            if (i + R <= r1) {
+                T vr[R * MM], wr[R * KK];
+                load_row<T, R * MM>(v + i * MM, vr);
+                load_row<T, R * KK>(w + i * KK, wr);
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int a = 0; a < MM; ++a)
+#pragma unroll
+                        for (int b = 0; b < KK; ++b)
+                            acc[a][b] = O::fma(O::conj(vr[r * MM + a]), wr[r * KK + b], acc[a][b]);
+            } else {
+                for (gidx j = i; j < r1; ++j) {
+                    T vr[MM], wr[KK];
+                    load(j, vr, wr);
+                    accum(vr, wr);
+                }
+            }
+        }
+        i = r1;  // nothing left for the row loops below
+    }
     if constexpr (UR > 1) {
         for (; i + gidx(UR - 1) * kT < r1; i += gidx(UR) * kT) {
             T vr[UR][MM], wr[UR][KK];
@@ -495,6 +547,46 @@ __global__ void __launch_bounds__(kT) tsmm_tile_kernel(T* __restrict__ w, gidx w
 // row, the V row and the W row moved with vector accesses, X broadcast from
 // shared memory; tmp[e] = sum over m ascending of V[i,m]*X[m,e], each product and
 // sum rounded separately (tsm.hpp:51-68).
+// R > 1: a thread computes R consecutive rows, moving their V and W rows with one vector
+// access each (1 x 1: four rows per LDG.256 / STG.256); same arithmetic per row.
+template <class T, int M, int K, int R>
+__device__ __forceinline__ void tsmm_rows_chunk(T* __restrict__ w, const T* __restrict__ v, const T* xs, gidx i,
+                                                T alpha, T beta, int beta_zero) {
+    using O = Ops<T>;
+    T vr[R * M], out[R * K];
+    load_row<T, R * M>(v + i * M, vr);
+    T old[R * K];
+    if (!beta_zero) load_row<T, R * K>(w + i * K, old);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        T tmp[K];
+#pragma unroll
+        for (int e = 0; e < K; ++e) tmp[e] = O::zero();
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+            for (int e = 0; e < K; ++e) tmp[e] = O::add(tmp[e], O::mul(vr[r * M + mm], xs[mm * K + e]));
+#pragma unroll
+        for (int e = 0; e < K; ++e)
+            out[r * K + e] = beta_zero ? O::mul(alpha, tmp[e]) : O::add(O::mul(alpha, tmp[e]), O::mul(beta, old[r * K + e]));
+    }
+    store_row<T, R * K>(w + i * K, out);
+}
+
+template <class T, int M, int K, int R>
+__global__ void __launch_bounds__(kT) tsmm_chunk_kernel(T* __restrict__ w, const T* __restrict__ v,
+                                                        const T* __restrict__ xcm, gidx n, T alpha, T beta,
+                                                        int beta_zero) {
+    __shared__ T xs[M * K];  // row-major
+    for (int t = threadIdx.x; t < M * K; t += kT) xs[t] = xcm[(t % K) * M + t / K];
+    __syncthreads();
+    const gidx nch = n / R;
+    for (gidx c = blockIdx.x * gidx(kT) + threadIdx.x; c < nch; c += gidx(gridDim.x) * kT)
+        tsmm_rows_chunk<T, M, K, R>(w, v, xs, c * R, alpha, beta, beta_zero);
+    if (blockIdx.x == 0 && threadIdx.x < n - nch * R)  // the last n % R rows one by one
+        tsmm_rows_chunk<T, M, K, 1>(w, v, xs, nch * R + threadIdx.x, alpha, beta, beta_zero);
+}
+
 template <class T, int M, int K>
 __global__ void __launch_bounds__(kT) tsmm_row_kernel(T* __restrict__ w, const T* __restrict__ v,
                                                       const T* __restrict__ xcm, gidx n, T alpha, T beta,
@@ -591,6 +683,25 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
                 }
                 if (used > 0) {
                     tsmttsm_final_kernel<T, false><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, used, m, k, xa, a, b);
+                    return 0;
+                }
+                // chunked path: 1 x 1 and 2 x 2 (double) with compact, 32-byte aligned rows
+                const bool chunk = SK_TSM_CHUNK && std::is_same_v<T, double> && !kahan && m == k && (m == 1 || m == 2) &&
+                                   vst == m && wst == k && reinterpret_cast<std::uintptr_t>(vp) % 32 == 0 &&
+                                   reinterpret_cast<std::uintptr_t>(wp) % 32 == 0;
+                if (chunk) {
+                    auto goc = [&]<int MK>() {
+                        constexpr int R = 32 / (MK * int(sizeof(T)));
+                        const gidx rp = (rows_per + R - 1) / R * R;  // CTA ranges start on a chunk
+                        const int np = int((n + rp - 1) / rp);
+                        tsmttsm_reg_kernel<T, MK, MK, false, R><<<np, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rp, p,
+                                                                                         pc);
+                        CK(cudaGetLastError());
+                        tsmttsm_final_kernel<T, false><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, np, m, k, xa,
+                                                                                                        a, b);
+                    };
+                    if (m == 1) goc.template operator()<1>();
+                    else goc.template operator()<2>();
                     return 0;
                 }
                 if (m <= 8 && k <= 8) {
@@ -713,6 +824,21 @@ void tsmm(DenseMat& w, const DenseMat& v_in, const DenseMat& x_in, const void* a
                     if (!exact && vst == m && wst == k && tsmm_dmma(wp, vp, xc, n, m, k, a, b, beta_zero, rt)) return 0;
                 }
                 auto pow2 = [](lidx q) { return q == 1 || q == 2 || q == 4 || q == 8; };
+                // 1 x 1 and 2 x 2 (double, 32-byte aligned): R rows per thread and vector access
+                if (SK_TSM_CHUNK && std::is_same_v<T, double> && m == k && (m == 1 || m == 2) && vst == m &&
+                    wst == k && reinterpret_cast<std::uintptr_t>(vp) % 32 == 0 &&
+                    reinterpret_cast<std::uintptr_t>(wp) % 32 == 0) {
+                    auto chunked = [&]<int MK>() {
+                        constexpr int R = 32 / (MK * int(sizeof(T)));
+                        const gidx nch = std::max<gidx>(1, n / R);
+                        const int grid = int(std::max<gidx>(1, std::min<gidx>((nch + kT - 1) / kT, gidx(rt.num_sms) * 8)));
+                        tsmm_chunk_kernel<T, MK, MK, R><<<grid, kT, 0, rt.stream>>>(wp, vp, xc, n, a, b,
+                                                                                  beta_zero ? 1 : 0);
+                    };
+                    if (m == 1) chunked.template operator()<1>();
+                    else chunked.template operator()<2>();
+                    return 0;
+                }
                 if (exact && pow2(m) && pow2(k) && vst == m && wst == k) {
                     const int grid = int(std::max<gidx>(1, std::min<gidx>((n + kT - 1) / kT, gidx(rt.num_sms) * 8)));
                     auto row = [&]<int M, int K>() {

@@ -194,3 +194,20 @@ def test_tsm_tensor_core_ragged_rows(sk, orc, m, k, n):
     want = orc.tsmm(V, X, W0, 1.5, 0.0) if n < 5000 else 1.5 * (V @ X)
     got = run_tsmm(sk, V, X, W0, 1.5, 0.0)
     assert np.max(np.abs(got - want) / (1 + np.abs(V) @ np.abs(X))) < 1e-12
+
+
+@pytest.mark.parametrize("mk", [1, 2])
+@pytest.mark.parametrize("n", [1, 3, 5, 1003, 4097, 300001])
+def test_tsm_chunked_narrow_ragged(sk, orc, mk, n):
+    """The 1 x 1 / 2 x 2 paths move R = 4 / 2 rows per 32-byte access; row counts that are
+    not multiples of R (and of the CTA ranges) end in a per-row tail.  TSMM stays
+    bit-identical to the reference order, TSMTTSM within 1e-12 * sum |v||w|."""
+    rng = np.random.default_rng(7 * n + mk)
+    V, W, X = rng.uniform(-1, 1, (n, mk)), rng.uniform(-1, 1, (n, mk)), rng.uniform(-1, 1, (mk, mk))
+    want = orc.tsmttsm(V, W, X, 0.75, 0.5)
+    got = run_tsmttsm(sk, V, W, X, 0.75, 0.5)
+    scale = np.abs(V).T @ np.abs(W)
+    assert np.all(np.abs(got - want) <= 1e-12 * (1 + scale + np.abs(X)))
+    W0 = rng.uniform(-1, 1, (n, mk))
+    for a, b in [(1.5, -0.5), (2.0, 0.0)]:
+        assert np.array_equal(run_tsmm(sk, V, X, W0, a, b), orc.tsmm(V, X, W0, a, b))
