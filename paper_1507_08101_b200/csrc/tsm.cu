@@ -279,6 +279,15 @@ __device__ __forceinline__ void store_row(T* p, const T (&r)[N]) {
 #ifndef SK_TSM_CHUNK    // 1: chunked paths for the 8- and 16-byte-row shapes (1x1, 2x2)
 #define SK_TSM_CHUNK 1
 #endif
+#ifndef SK_TSM_PAIR8    // 1: TSMTTSM 8 x 8 with a lane pair per row (32 accumulators per lane)
+#define SK_TSM_PAIR8 1
+#endif
+#ifndef SK_TT_PAIR_UR
+#define SK_TT_PAIR_UR 2
+#endif
+#ifndef SK_TT_SPLIT_LPR  // lanes per row of the 8 x 8 split kernel
+#define SK_TT_SPLIT_LPR 2
+#endif
 
 // TSMTTSM, m <= MM, k <= KK (MM, KK in {1,2,4,8}): each thread keeps the whole
 // m x k block in registers and walks its rows of the CTA's contiguous range;
@@ -435,6 +444,71 @@ __global__ void __launch_bounds__(kT) tsmttsm_reg_kernel(const T* __restrict__ v
             partial[gidx(blockIdx.x) * m * k + cell] = s;
             if constexpr (KAHAN) pcomp[gidx(blockIdx.x) * m * k + cell] = c;
         }
+    }
+}
+
+// TSMTTSM 8 x 8 (double, compact rows; measured 2.40 -> 2.35 ms at N = 1e8 with LPR = 2,
+// UR = 2; LPR = 4 / 8 and UR = 4 no better, profiles r2ac): LPR lanes share a row -- lane q of the group
+// keeps the (8/LPR) x 8 slice of the cell block for V columns q*8/LPR.., loads its slice of
+// the V row and the whole W row (the group's identical W addresses merge into one
+// request), so a lane holds 8*8/LPR accumulators instead of 64 (more lanes resident, more
+// rows in flight); UR rows per lane per batch.
+template <int LPR, int UR>
+__global__ void __launch_bounds__(kT) tsmttsm_split8_kernel(const double* __restrict__ v, const double* __restrict__ w,
+                                                            gidx n, gidx rows_per_cta, double* partial) {
+    constexpr int MA = 8 / LPR;  // V columns (cell rows) per lane
+    __shared__ double red[kT / 32][64];
+    double acc[MA][8];
+#pragma unroll
+    for (int a = 0; a < MA; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    const int q = threadIdx.x % LPR;
+    const gidx r0 = gidx(blockIdx.x) * rows_per_cta;
+    const gidx r1 = min(n, r0 + rows_per_cta);
+    constexpr int kRowsPerPass = kT / LPR;
+    gidx i = r0 + threadIdx.x / LPR;
+    for (; i + gidx(UR - 1) * kRowsPerPass < r1; i += gidx(UR) * kRowsPerPass) {
+        double vr[UR][MA], wr[UR][8];
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+            load_row<double, MA>(v + (i + gidx(u) * kRowsPerPass) * 8 + MA * q, vr[u]);
+            load_row<double, 8>(w + (i + gidx(u) * kRowsPerPass) * 8, wr[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+#pragma unroll
+            for (int a = 0; a < MA; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[a][b] = fma(vr[u][a], wr[u][b], acc[a][b]);
+    }
+    for (; i < r1; i += kRowsPerPass) {
+        double vr[MA], wr[8];
+        load_row<double, MA>(v + i * 8 + MA * q, vr);
+        load_row<double, 8>(w + i * 8, wr);
+#pragma unroll
+        for (int a = 0; a < MA; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = fma(vr[a], wr[b], acc[a][b]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < MA; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+#pragma unroll
+            for (int s = 16; s >= LPR; s >>= 1) acc[a][b] += __shfl_xor_sync(0xffffffffu, acc[a][b], s);
+    if (lane < LPR) {
+#pragma unroll
+        for (int a = 0; a < MA; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) red[warp][b * 8 + MA * q + a] = acc[a][b];  // col-major 8 x 8
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        double s = 0.0;
+        for (int t = 0; t < kT / 32; ++t) s += red[t][threadIdx.x];
+        partial[gidx(blockIdx.x) * 64 + threadIdx.x] = s;
     }
 }
 
@@ -702,6 +776,16 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
                     };
                     if (m == 1) goc.template operator()<1>();
                     else goc.template operator()<2>();
+                    return 0;
+                }
+                if (SK_TSM_PAIR8 && std::is_same_v<T, double> && !kahan && m == 8 && k == 8 && vst == 8 && wst == 8 &&
+                    reinterpret_cast<std::uintptr_t>(vp) % 32 == 0 && reinterpret_cast<std::uintptr_t>(wp) % 32 == 0) {
+                    if constexpr (std::is_same_v<T, double>) {
+                        tsmttsm_split8_kernel<SK_TT_SPLIT_LPR, SK_TT_PAIR_UR><<<nparts, kT, 0, rt.stream>>>(vp, wp, n, rows_per, p);
+                        CK(cudaGetLastError());
+                        tsmttsm_final_kernel<T, false><<<int((cells + 127) / 128), 128, 0, rt.stream>>>(p, pc, nparts, m,
+                                                                                                        k, xa, a, b);
+                    }
                     return 0;
                 }
                 if (m <= 8 && k <= 8) {
