@@ -698,7 +698,7 @@ __device__ __forceinline__ void slot_add(T* p, T v) {
 // 5.0 vs 6.2 ms).
 template <class T, int W>
 constexpr bool dots_in_registers() {
-    return SK_DOTS_REG != 0 && (SK_DOTS_REG == 2 || (std::is_same_v<T, double> && (W == 4 || W == 32)));
+    return SK_DOTS_REG != 0 && (SK_DOTS_REG >= 2 || (std::is_same_v<T, double> && (W == 4 || W == 32)));
 }
 template <int K, int M, int TPR>
 constexpr int rs_final() {
@@ -1051,10 +1051,13 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
         constexpr int NCL = kNCW * 32;
         constexpr bool kDR = dots_in_registers<T, W>();
         constexpr int KD = 3 * VEC;                       // dot terms per lane and row
-        constexpr int KF = rs_final<KD, 16, TPR>();        // register accumulators per lane
+        // SK_DOTS_REG == 3: every lane keeps all KD terms of its rows (no per-pass shuffles),
+        // reduced over the row slots once at the end
+        constexpr bool kDirect = kDR && SK_DOTS_REG == 3;
+        constexpr int KF = kDirect ? KD : rs_final<KD, 16, TPR>();  // register accumulators per lane
         T dreg[kDR && DOTS ? KF : 1];
         int dbase = 0, dvalid = KD;                        // slice of the KD terms this lane keeps
-        if constexpr (DOTS && kDR) rs_slice<KD, 16, TPR>(lane, dbase, dvalid);
+        if constexpr (DOTS && kDR && !kDirect) rs_slice<KD, 16, TPR>(lane, dbase, dvalid);
         if constexpr (DOTS && kDR) {
 #pragma unroll
             for (int q = 0; q < KF; ++q) dreg[q] = O::zero();
@@ -1265,7 +1268,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             }
             if constexpr (DOTS && kDR) {
                 // warp-uniform: sum the pass's rows slot-wise, keep this lane's slice
-                rs_step<T, KD, 16, TPR>(dt, lane);
+                if constexpr (!kDirect) rs_step<T, KD, 16, TPR>(dt, lane);
 #pragma unroll
                 for (int q = 0; q < KF; ++q) dreg[q] = O::add(dreg[q], dt[q]);
             }
@@ -1273,7 +1276,16 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // matrix data of the tile consumed
         }
-        if constexpr (DOTS && kDR) {
+        if constexpr (DOTS && kDirect) {
+            // lanes of a row slot -> warp total per column (fixed butterfly order)
+#pragma unroll
+            for (int q = 0; q < KD; ++q) {
+                T v = dreg[q];
+#pragma unroll
+                for (int m = TPR; m < 32; m <<= 1) v = O::add(v, shfl_xor(v, m));
+                if (lane < TPR) red[warp][q / VEC][lane * VEC + q % VEC] = v;
+            }
+        } else if constexpr (DOTS && kDR) {
             // every (dot, column) lives in exactly one lane of the warp: its warp total
 #pragma unroll
             for (int q = 0; q < KF; ++q) {
