@@ -840,6 +840,9 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 #ifndef SK_DYN_DOTS  // experiment: dynamic tiles for the dots kernels (dots then depend on timing)
 #define SK_DYN_DOTS 0
 #endif
+#ifndef SK_DYN_PLAIN  // dynamic tiles for the epilogue-free kernels (when the launch rule below says so)
+#define SK_DYN_PLAIN 1
+#endif
 
 #ifndef SK_RMINB
 #define SK_RMINB 4
@@ -897,7 +900,9 @@ constexpr std::size_t rows_smem_bytes() {
            128;
 }
 
-template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED>
+// DYN: the kernel can take its tiles from a.tile_counter (dynamic deal); a separate
+// instantiation so the static epilogue-free kernel keeps its register schedule.
+template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED, bool DYN>
 __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double> && W == 1 ? SK_RMINB_DOTS_NARROW
                                                                                          : SK_RMINB_DOTS)
                                                     : SK_RMINB)
@@ -942,9 +947,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
     // CTA sweeps a tile): the producer takes the next tile from a global counter, so
     // the sweep front stays one contiguous band (x reuse) and no CTA trails at the end;
     // a tile index >= ntiles in the stage header tells the consumers to stop
-    // (measured, tools/ab_plain.sh r2v: 400^3 w = 8 AXPBY 3.35 -> 2.71 ms; the plain
-    // epilogue-free kernels keep the static deal, 2.40 vs 2.47 ms, C1 22 vs 25 us)
-    constexpr bool kDynOK = SK_DYN_TILES && (!DOTS || SK_DYN_DOTS) && !PLAIN;
+    // (measured, r2v / r2w: 400^3 w = 8 AXPBY 3.35 -> 2.71 ms; the epilogue-free kernels
+    // by the launch rule in launch_tma_rows)
+    constexpr bool kDynOK = DYN && SK_DYN_TILES;
     const bool dyn = kDynOK && a.tile_counter != nullptr;
     if (warp == kNCW) {
         // ------------------------------------------------- producer warp (as spmv_tma_kernel)
@@ -1512,13 +1517,13 @@ inline int rows_mode() {
     return mode;
 }
 
-template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false>
+template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false,
+          bool DYN = (!DOTS || SK_DYN_DOTS) && !PLAIN && SK_DYN_TILES>
 LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     KArgs<T> a = a_in;
-    if ((DOTS && !SK_DYN_DOTS) || PLAIN || !SK_DYN_TILES) a.tile_counter = nullptr;
-    if (a.tile_counter) CK(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st));
+    if (!DYN) a.tile_counter = nullptr;
     constexpr int U = rows_unroll<T, W, DOTS>();
-    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED>;
+    auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED, DYN>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
     static std::atomic<std::uint64_t> attr_devs{0};
     smem_attr_per_device(kern, smem, rt.device, attr_devs);
@@ -1536,6 +1541,15 @@ LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cu
         const char* e = std::getenv("SELLKIT_TMA_SEG");
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
+    // Epilogue-free sweeps deal tiles statically unless the static deal drifts: with many
+    // tiles per CTA the CTAs' fronts spread apart and x falls out of L2 (400^3 w = 8: 10.51
+    // vs 9.50 GB read, 2.29-2.32 -> 2.08-2.19 ms); smaller sweeps pay for the counter
+    // instead (C1 21 -> 25 us, 256^3 w = 8 +2.6 %; wider RHS rows: within noise; r2ak, r2am)
+    if constexpr (PLAIN && !DYN && SK_DYN_PLAIN && SK_DYN_TILES && std::is_same_v<T, double>) {
+        if (a_in.tile_counter && ntiles >= 600 * gidx(grid))
+            return launch_tma_rows<T, C, W, DOTS, PLAIN, MAPPED, true>(a_in, rgt, rt, st);
+    }
+    if (a.tile_counter) CK(cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st));
     kern<<<grid, kTmaThreads, smem, st>>>(a, rgt, ntiles, seg);
     return {grid, grid, 0};
 }
