@@ -308,13 +308,18 @@ def run_ours(args, rank, world, local_rank):
     if job is None:
         crs = sk.crs_stencil(7, n)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        A = crs.build(args.chunk, args.sigma)           # synchronous: SELL-C-sigma built on the GPU
-        t_build = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        sk.call("sellkit_mat_update_values", A.h, crs.h)  # constant-pattern value refresh
-        t_update = time.perf_counter() - t0
-        build = {"build_ms": t_build * 1e3, "update_values_ms": t_update * 1e3}
+        t_builds, t_updates = [], []
+        for rep in range(3):  # the first build also pays the process's first big allocations
+            t0 = time.perf_counter()
+            A = crs.build(args.chunk, args.sigma)           # synchronous: SELL-C-sigma built on the GPU
+            t_builds.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            sk.call("sellkit_mat_update_values", A.h, crs.h)  # constant-pattern value refresh
+            t_updates.append(time.perf_counter() - t0)
+            if rep < 2:
+                del A
+        build = {"build_ms": float(np.median(t_builds)) * 1e3, "update_values_ms": float(np.median(t_updates)) * 1e3,
+                 "build_ms_each": [t * 1e3 for t in t_builds]}
         del crs
         rows_local = N
         x = sk.densemat(N, w)
@@ -449,8 +454,9 @@ def run_ours(args, rank, world, local_rank):
         # the paper's construction metric (perfmodel.cpp:41-45): cost in SpMV units
         build["spmv_units_build"] = build["build_ms"] / ms_per_step
         build["spmv_units_update_values"] = build["update_values_ms"] / ms_per_step
-        build["what"] = ("wall time of the synchronous sellkit_mat_build (CRS in HBM -> SELL-C-sigma: sigma-sort, "
-                         "permutation, chunk lengths/offsets, fill) and sellkit_mat_update_values, over ms_per_step")
+        build["what"] = ("median wall time of 3 synchronous sellkit_mat_build calls (CRS in HBM -> SELL-C-sigma: "
+                         "sigma-sort, permutation, chunk lengths/offsets, fill) and sellkit_mat_update_values, over "
+                         "ms_per_step")
         line["construction"] = build
     print(json.dumps(line), flush=True)
 
