@@ -416,6 +416,10 @@ void spmv_device(DenseMat& y, const SellMat& A, const DenseMat& x, const SpmvOpt
         T* res = gl + W;
         a.partial = res + 3 * W;
         a.tile_counter = reinterpret_cast<int*>(sc + need - 256);  // zeroed per launch when used
+#if SK_CHECK
+        a.xrows = x.nrows;
+        a.slots = A.slots;
+#endif
         if (o.flags & kFlagVshift) {
             CK(cudaMemcpyAsync(gl, o.gamma_list, W * es, cudaMemcpyDefault, st));
             a.gamma_list = gl;

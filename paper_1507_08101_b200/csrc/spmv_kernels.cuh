@@ -75,7 +75,30 @@ struct KArgs {
                              // concurrent halo pack on the communication stream)
     int* tile_counter;       // rows kernels without dots: tiles handed out by an atomic counter
                              // (zeroed before the launch) instead of a static round robin
+#if SK_CHECK
+    lidx xrows;              // checked build: rows of x (gather bound)
+    gidx slots;              // checked build: stored slots of the matrix
+#endif
 };
+
+// Checked build (make EXTRA_NVFLAGS=-DSK_CHECK=1, tools/check_build.sh): device-side bounds
+// assertions on every gather index and matrix range -- the stand-in for compute-sanitizer's
+// memcheck, which is closed on this pool.
+#ifndef SK_CHECK
+#define SK_CHECK 0
+#endif
+#if SK_CHECK
+#define SK_DEVICE_CHECK(cond, what)                                                                    \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("[sellkit check] %s failed: %s (block %d thread %d)\n", what, #cond, int(blockIdx.x), \
+                   int(threadIdx.x));                                                                  \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#else
+#define SK_DEVICE_CHECK(cond, what) ((void)0)
+#endif
 
 namespace spmv_detail {
 
@@ -504,6 +527,10 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
             for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
             for (int q = lane; q < nc; q += 32) hdr[s].hlen[q] = a.chunk_len[c0 + q];
             const gidx nslots = a.chunk_offset[c1] - off0;
+#if SK_CHECK
+            SK_DEVICE_CHECK(c0 <= c1 && c1 <= a.nchunks, "tma kernel: tile chunk range");
+            SK_DEVICE_CHECK(off0 >= 0 && off0 + nslots <= a.slots, "tma kernel: tile slot range");
+#endif
             const bool fits = nslots <= SCAP;
             if (lane == 0) {
                 hdr[s].overflow = fits ? 0 : 1;
@@ -1009,6 +1036,10 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             for (int q = lane; q <= nc; q += 32) hdr[s].hoff[q] = int(a.chunk_offset[c0 + q] - off0);
             for (int q = lane; q < nc; q += 32) hdr[s].hlen[q] = a.chunk_len[c0 + q];
             const gidx nslots = a.chunk_offset[c1] - off0;
+#if SK_CHECK
+            SK_DEVICE_CHECK(c0 <= c1 && c1 <= a.nchunks, "rows kernel: tile chunk range");
+            SK_DEVICE_CHECK(off0 >= 0 && off0 + nslots <= a.slots, "rows kernel: tile slot range");
+#endif
             const bool fits = nslots <= SCAP;
             if (lane == 0) {
                 hdr[s].overflow = fits ? 0 : 1;
@@ -1122,6 +1153,9 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 vp += off;
                 cp += off;
                 auto xrow = [&](lidx c) -> const T* {
+#if SK_CHECK
+                    SK_DEVICE_CHECK(unsigned(c) < unsigned(a.xrows), "rows kernel: RHS row index in range");
+#endif
                     return reinterpret_cast<const T*>(xbytes + (unsigned long long)unsigned(c) * xstride);
                 };
                 auto ldx = [&](const T* p) -> Vec<T, VEC> {
@@ -1354,6 +1388,9 @@ __global__ void __launch_bounds__(kBlock) spmv_generic_kernel(const KArgs<T> a) 
         for (lidx j = 0; j < cl; ++j) {
             const gidx slot = off + gidx(j) * a.C + i;
             const T v = a.val[slot];
+#if SK_CHECK
+            SK_DEVICE_CHECK(slot < a.slots && unsigned(a.col[slot]) < unsigned(a.xrows), "generic kernel: slot / column");
+#endif
             const T* xr = a.x + gidx(a.col[slot]) * a.x_rs + gidx(cb0) * a.x_cs;
 #pragma unroll
             for (int e = 0; e < kGW; ++e)
