@@ -1,0 +1,45 @@
+"""bench.py contract checks that need no GPU: the reference arm on a small full matrix
+(same config as the GPU line, one JSON line with the required keys) and the refusal to
+fake a multi-GPU run on a box without the GPUs."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args, env=None, timeout=600):
+    e = dict(os.environ)
+    e.update(env or {})
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE"):
+        e.pop(k, None)
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=timeout, cwd=ROOT, env=e)
+
+
+def test_reference_arm_json_line():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libsellkit.so")):
+        pytest.skip("reference library not built")
+    r = _run("--impl", "reference", "--n", "24", "--steps", "2", "--warmup", "1", env={"OMP_NUM_THREADS": "2"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["config"]["same_config"] is True
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["construction"]["spmv_units_build"] > 0
+
+
+def test_multi_gpu_request_needs_the_gpus():
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("this box has the GPUs")
+    r = _run("--gpus", "2", "--steps", "1", "--warmup", "1", timeout=300)
+    assert r.returncode != 0
+    assert "needs 2 visible GPUs" in r.stderr
