@@ -88,6 +88,9 @@ int main() {
     cudaMalloc(&t, big);
     cudaMemset(t, 1, big);
     cudaDeviceSynchronize();
+    sweep<256>(t, unsigned((64u << 10) / 256), "L1 64KB", sms, clk);
+    sweep<128>(t, unsigned((64u << 10) / 128), "L1 64KB", sms, clk);
+    sweep<64>(t, unsigned((64u << 10) / 64), "L1 64KB", sms, clk);
     sweep<256>(t, unsigned(small / 256), "L2 48MB", sms, clk);
     sweep<128>(t, unsigned(small / 128), "L2 48MB", sms, clk);
     sweep<64>(t, unsigned(small / 64), "L2 48MB", sms, clk);
