@@ -178,3 +178,33 @@ def test_dist_timeline_trace(sk):
         for o in (r - 1, r + 1):
             if 0 <= o < k:
                 assert t[o][1] <= re_, (r, o, t)
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_dist_col_major_vectors(sk, k):
+    """Distributed vectors in column-major order (sellkit_dvec_create order argument): the
+    pack kernel and the generic sweeps take the strides, so y, z and the dots equal the
+    row-major run bit for bit (same per-row order)."""
+    n, w = 10, 3
+    N = n ** 3
+    rp, c, v = stencil_crs(7, n)
+    ctx = dist.DistContext(sk, sk.crs(rp, c, v), k, 4, 8, record=False)
+    xv, y0, z0 = hash_block(N, w, 31), hash_block(N, w, 32), hash_block(N, w, 33)
+    flags = (sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX |
+             sellkit.CHAIN_AXPBY)
+    out = {}
+    for order in (sellkit.ROW_MAJOR, sellkit.COL_MAJOR):
+        dx, dy, dz = ctx.vec(w, order), ctx.vec(w, order), ctx.vec(w, order)
+        for arr, dv in [(xv, dx), (y0, dy), (z0, dz)]:
+            ctx.scatter(sk.densemat_from(arr), dv)
+        dots = np.zeros(3 * w)
+        ctx.spmv(dy, dx, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, delta=1.0, eta=0.3, z=dz, dot=dots)
+        yg, zg = sk.densemat(N, w), sk.densemat(N, w)
+        ctx.gather(dy, yg)
+        ctx.gather(dz, zg)
+        out[order] = (yg.copy_out(), zg.copy_out(), dots)
+    yr, zr, dr = out[sellkit.ROW_MAJOR]
+    yc, zc, dc = out[sellkit.COL_MAJOR]
+    assert np.array_equal(yr, yc) and np.array_equal(zr, zc)
+    sc = np.concatenate([np.sum(yr ** 2, 0), np.sum(np.abs(xv * yr), 0), np.sum(xv ** 2, 0)])
+    assert np.all(np.abs(dr - dc) <= 1e-12 * (1 + sc))
