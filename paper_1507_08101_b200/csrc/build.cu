@@ -63,20 +63,79 @@ __global__ void iota_kernel(lidx* out, lidx n) {
 // sigma_permutation (sellcs.hpp:80-91) for scopes that fit shared memory: one
 // CTA per scope; the stable descending rank of element i is
 // #{j : len_j > len_i} + #{j < i : len_j == len_i}.
-__global__ void scope_sort_kernel(const lidx* lens, lidx n, lidx sigma, lidx* order) {
+// Scopes whose rows are all shorter than kSortLMax (stencils, lattices) count instead of
+// comparing: a length histogram gives the first term, and for the second the elements are
+// walked in index order, 256 at a time -- lanes of equal length within a warp rank by
+// __match_any_sync, earlier warps of the chunk and earlier chunks by per-length counts.
+// O(scope) instead of O(scope^2) work (400^3: 3.2 ms of the build).
+constexpr int kSortLMax = 63;
+constexpr int kSortThreads = 256;
+
+__global__ void __launch_bounds__(kSortThreads) scope_sort_kernel(const lidx* lens, lidx n, lidx sigma, lidx* order) {
     extern __shared__ lidx sl[];
+    __shared__ int hist[kSortLMax + 1];
+    __shared__ int greater[kSortLMax + 1];
+    __shared__ int run[kSortLMax + 1];
+    __shared__ int wcnt[kSortThreads / 32][kSortLMax + 1];
+    __shared__ int big;
     const gidx s0 = gidx(blockIdx.x) * sigma;
     const lidx cnt = lidx(std::min<gidx>(sigma, gidx(n) - s0));
-    for (lidx i = threadIdx.x; i < cnt; i += blockDim.x) sl[i] = lens[s0 + i];
+    if (threadIdx.x <= kSortLMax) {
+        hist[threadIdx.x] = 0;
+        run[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) big = 0;
     __syncthreads();
     for (lidx i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const lidx li = sl[i];
-        lidx rank = 0;
-        for (lidx j = 0; j < cnt; ++j) {
-            const lidx lj = sl[j];
-            rank += (lj > li) || (lj == li && j < i);
+        const lidx l = lens[s0 + i];
+        sl[i] = l;
+        if (l > kSortLMax || l < 0) big = 1;
+        else atomicAdd(&hist[l], 1);
+    }
+    __syncthreads();
+    if (big) {  // long rows in this scope: the comparison rank
+        for (lidx i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const lidx li = sl[i];
+            lidx rank = 0;
+            for (lidx j = 0; j < cnt; ++j) {
+                const lidx lj = sl[j];
+                rank += (lj > li) || (lj == li && j < i);
+            }
+            order[s0 + rank] = lidx(s0 + i);
         }
-        order[s0 + rank] = lidx(s0 + i);
+        return;
+    }
+    if (threadIdx.x <= kSortLMax) {
+        int g = 0;
+        for (int m = threadIdx.x + 1; m <= kSortLMax; ++m) g += hist[m];
+        greater[threadIdx.x] = g;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    __syncthreads();
+    for (lidx base = 0; base < cnt; base += kSortThreads) {
+        const lidx i = base + lidx(threadIdx.x);
+        const bool valid = i < cnt;
+        const int l = valid ? int(sl[i]) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, l);
+        const int in_warp = __popc(peers & lt);
+        wcnt[warp][lane] = 0;
+        wcnt[warp][lane + 32] = 0;
+        __syncwarp();
+        if (valid && in_warp == 0) wcnt[warp][l] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            int before = 0;
+            for (int w = 0; w < warp; ++w) before += wcnt[w][l];
+            order[s0 + greater[l] + run[l] + before + in_warp] = lidx(s0 + i);
+        }
+        __syncthreads();
+        if (threadIdx.x <= kSortLMax) {
+            int t = 0;
+            for (int w = 0; w < kSortThreads / 32; ++w) t += wcnt[w][threadIdx.x];
+            run[threadIdx.x] += t;
+        }
+        __syncthreads();
     }
 }
 
@@ -352,7 +411,7 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
         const lidx scope = lidx(std::min<gidx>(sigma, n));
         if (scope <= 4096) {
             const gidx nscopes = (gidx(n) + scope - 1) / scope;
-            scope_sort_kernel<<<unsigned(nscopes), 256, std::size_t(scope) * sizeof(lidx), rt.stream>>>(
+            scope_sort_kernel<<<unsigned(nscopes), kSortThreads, std::size_t(scope) * sizeof(lidx), rt.stream>>>(
                 lens.as<lidx>(), n, scope, pinv);
         } else {
             DeviceBuffer mx(sizeof(int), a.device);

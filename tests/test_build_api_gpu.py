@@ -156,3 +156,22 @@ def test_apply_override_matrix_free(sk):
     sk.call("sellkit_ext_mat_set_apply_override", A.h, None, None)
     sk.spmv(y, A, x)
     assert y.copy_out()[:, 0].tolist() == [1.0, 2.0, 3.0]
+
+
+@pytest.mark.parametrize("sigma,maxlen", [(256, 13), (4096, 63), (4096, 64), (1000, 200), (36, 5)])
+def test_sigma_permutation_stable_descending(sk, sigma, maxlen):
+    """The σ-sort (sellcs.hpp:80-91): within each scope, rows stably ordered by descending
+    length -- both the counting path (all rows < 64 entries) and the comparison path, ties,
+    several 256-row chunks per scope and a ragged last scope."""
+    rng = np.random.default_rng(sigma + maxlen)
+    n = 3 * sigma + sigma // 3 + 1
+    lens = rng.integers(0, maxlen + 1, n)
+    lens[rng.integers(0, n, n // 8)] = maxlen  # many ties at the top length
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    step = n // (maxlen + 1)
+    col = np.concatenate([(r % step) + step * np.arange(l) for r, l in enumerate(lens)]).astype(np.int64)
+    val = rng.standard_normal(int(rp[-1]))
+    A = sk.crs(rp, col, val).build(4, sigma)
+    pinv = A.export()["row_perm_inv"]
+    want = np.concatenate([s0 + np.argsort(-lens[s0:s0 + sigma], kind="stable") for s0 in range(0, n, sigma)])
+    assert np.array_equal(pinv[:n], want)
