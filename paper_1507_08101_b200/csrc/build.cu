@@ -71,7 +71,8 @@ __global__ void iota_kernel(lidx* out, lidx n) {
 constexpr int kSortLMax = 63;
 constexpr int kSortThreads = 256;
 
-__global__ void __launch_bounds__(kSortThreads) scope_sort_kernel(const lidx* lens, lidx n, lidx sigma, lidx* order) {
+__global__ void __launch_bounds__(kSortThreads) scope_sort_kernel(const gidx* __restrict__ rowptr, lidx n, lidx sigma,
+                                                                  lidx* __restrict__ order) {
     extern __shared__ lidx sl[];
     __shared__ int hist[kSortLMax + 1];
     __shared__ int greater[kSortLMax + 1];
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(kSortThreads) scope_sort_kernel(const lidx* le
     if (threadIdx.x == 0) big = 0;
     __syncthreads();
     for (lidx i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const lidx l = lens[s0 + i];
+        const lidx l = lidx(rowptr[s0 + i + 1] - rowptr[s0 + i]);
         sl[i] = l;
         if (l > kSortLMax || l < 0) big = 1;
         else atomicAdd(&hist[l], 1);
@@ -164,17 +165,41 @@ __global__ void max_kernel(const lidx* v, gidx n, int* out) {
     if (threadIdx.x == 0) atomicMax(out, red[0]);
 }
 
-// row_perm[row_perm_inv[k]] = k ; rowlen[k] = lens[row_perm_inv[k]] (sellcs.hpp:169-177)
-__global__ void perm_kernel(const lidx* perm_inv, const lidx* lens, lidx n, lidx n_pad, lidx* perm,
-                            lidx* rowlen) {
+// row_perm[row_perm_inv[k]] = k ; rowlen[k] = len(row_perm_inv[k]) (sellcs.hpp:169-177).
+// FUSED (C divides 32): a chunk is C consecutive lanes of one warp, so the chunk
+// length (sellcs.hpp:179-186) is a segmented warp max and chunk_len_kernel is skipped.
+template <bool FUSED>
+__global__ void perm_kernel(const lidx* __restrict__ perm_inv, const gidx* __restrict__ rowptr, lidx n, lidx n_pad,
+                            lidx C, lidx* __restrict__ perm, lidx* __restrict__ rowlen, lidx* __restrict__ chunk_len,
+                            gidx* __restrict__ sizes, gidx nchunks, int* maxlen) {
+    __shared__ int red[kThreads / 32];
+    const int lane = threadIdx.x & 31;
     const gidx k = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
-    if (k >= n_pad) return;
+    lidx len = 0;
     if (k < n) {
         const lidx o = perm_inv[k];
         perm[o] = lidx(k);
-        rowlen[k] = lens[o];
-    } else {
-        rowlen[k] = 0;
+        len = lidx(rowptr[o + 1] - rowptr[o]);
+    }
+    if (k < n_pad) rowlen[k] = len;
+    if constexpr (FUSED) {
+        if (k == nchunks * C) sizes[nchunks] = 0;
+        lidx lc = len;
+        for (int d = 1; d < C; d <<= 1) lc = max(lc, __shfl_xor_sync(0xffffffffu, lc, d));
+        if (k < n_pad && lane % C == 0) {
+            const gidx c = k / C;
+            chunk_len[c] = lc;
+            sizes[c] = gidx(C) * lc;
+        }
+        for (int d = 16; d >= 1; d >>= 1) lc = max(lc, __shfl_xor_sync(0xffffffffu, lc, d));
+        if (lane == 0) red[threadIdx.x >> 5] = lc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int m = 0;
+            for (int w = 0; w < kThreads / 32; ++w) m = max(m, red[w]);
+            // one atomic per CTA, and only while it raises the maximum
+            if (m > *reinterpret_cast<volatile int*>(maxlen)) atomicMax(maxlen, m);
+        }
     }
 }
 
@@ -197,9 +222,11 @@ __global__ void chunk_len_kernel(const lidx* rowlen, gidx nchunks, lidx C, lidx*
 // Chunk fill (sellcs.hpp:193-229), one thread per stored row: writes every
 // slot j < chunk_len of its row, padding with value 0 / column 0.
 template <class T>
-__global__ void fill_kernel(const gidx* rowptr, const gidx* ccol, const T* cval, const lidx* perm_inv,
-                            const lidx* perm, const lidx* rowlen, const lidx* chunk_len, const gidx* chunk_offset,
-                            lidx n, lidx n_pad, lidx C, gidx ncols, int permute, T* val, lidx* col, int* err) {
+__global__ void fill_kernel(const gidx* __restrict__ rowptr, const gidx* __restrict__ ccol, const T* __restrict__ cval,
+                            const lidx* __restrict__ perm_inv, const lidx* __restrict__ perm,
+                            const lidx* __restrict__ rowlen, const lidx* __restrict__ chunk_len,
+                            const gidx* __restrict__ chunk_offset, lidx n, lidx n_pad, lidx C, gidx ncols, int permute,
+                            T* __restrict__ val, lidx* __restrict__ col, int* err) {
     const gidx k = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
     if (k >= n_pad) return;
     const gidx c = k / C;
@@ -213,6 +240,7 @@ __global__ void fill_kernel(const gidx* rowptr, const gidx* ccol, const T* cval,
         src = rowptr[perm_inv[k]];
     }
     int bad = 0;
+#pragma unroll 4
     for (lidx j = 0; j < cl; ++j) {
         const gidx slot = off + gidx(j) * C + i;
         if (j < len) {
@@ -232,8 +260,10 @@ __global__ void fill_kernel(const gidx* rowptr, const gidx* ccol, const T* cval,
 
 // update_values (sellcs.hpp:269-284), one thread per original row.
 template <class T>
-__global__ void update_values_kernel(const gidx* rowptr, const T* cval, const lidx* perm, const lidx* rowlen,
-                                     const gidx* chunk_offset, lidx n, lidx C, T* val, int* err) {
+__global__ void update_values_kernel(const gidx* __restrict__ rowptr, const T* __restrict__ cval,
+                                     const lidx* __restrict__ perm, const lidx* __restrict__ rowlen,
+                                     const gidx* __restrict__ chunk_offset, lidx n, lidx C, T* __restrict__ val,
+                                     int* err) {
     const gidx o = blockIdx.x * gidx(blockDim.x) + threadIdx.x;
     if (o >= n) return;
     const lidx stored = perm[o];
@@ -246,6 +276,7 @@ __global__ void update_values_kernel(const gidx* rowptr, const T* cval, const li
     const gidx c = stored / C;
     const lidx i = stored - lidx(c * C);
     const gidx base = chunk_offset[c];
+#pragma unroll 4
     for (lidx j = 0; j < len; ++j) val[base + gidx(j) * C + i] = cval[b + j];
 }
 
@@ -397,9 +428,6 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
     m->device = a.device;
     m->nnz = a.nnz;
 
-    DeviceBuffer lens(std::size_t(n) * sizeof(lidx), a.device);
-    row_lengths_kernel<<<blocks_for(n), kThreads, 0, rt.stream>>>(a.rowptr.as<gidx>(), n, lens.as<lidx>());
-    CK(cudaGetLastError());
 
     m->row_perm_inv = DeviceBuffer(std::size_t(n) * sizeof(lidx), a.device);
     lidx* pinv = m->row_perm_inv.as<lidx>();
@@ -412,8 +440,10 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
         if (scope <= 4096) {
             const gidx nscopes = (gidx(n) + scope - 1) / scope;
             scope_sort_kernel<<<unsigned(nscopes), kSortThreads, std::size_t(scope) * sizeof(lidx), rt.stream>>>(
-                lens.as<lidx>(), n, scope, pinv);
+                a.rowptr.as<gidx>(), n, scope, pinv);
         } else {
+            DeviceBuffer lens(std::size_t(n) * sizeof(lidx), a.device);
+            row_lengths_kernel<<<blocks_for(n), kThreads, 0, rt.stream>>>(a.rowptr.as<gidx>(), n, lens.as<lidx>());
             DeviceBuffer mx(sizeof(int), a.device);
             CK(cudaMemsetAsync(mx.get(), 0, sizeof(int), rt.stream));
             max_kernel<<<std::min(blocks_for(n), rt.num_sms * 4), kThreads, 0, rt.stream>>>(lens.as<lidx>(), n,
@@ -448,25 +478,37 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
     m->nrows_padded = lidx(nchunks * C);
     m->row_perm = DeviceBuffer(std::size_t(n) * sizeof(lidx), a.device);
     m->rowlen = DeviceBuffer(std::size_t(m->nrows_padded) * sizeof(lidx), a.device);
-    perm_kernel<<<blocks_for(m->nrows_padded), kThreads, 0, rt.stream>>>(pinv, lens.as<lidx>(), n, m->nrows_padded,
-                                                                         m->row_perm.as<lidx>(), m->rowlen.as<lidx>());
-    CK(cudaGetLastError());
-
     m->chunk_len = DeviceBuffer(std::size_t(nchunks) * sizeof(lidx), a.device);
     m->chunk_offset = DeviceBuffer(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
     {
         DeviceBuffer sizes(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
-        DeviceBuffer mx(sizeof(int), a.device);
-        CK(cudaMemsetAsync(mx.get(), 0, sizeof(int), rt.stream));
-        chunk_len_kernel<<<blocks_for(nchunks + 1), kThreads, 0, rt.stream>>>(
-            m->rowlen.as<lidx>(), nchunks, C, m->chunk_len.as<lidx>(), sizes.as<gidx>(), mx.as<int>());
+        DeviceBuffer out(2 * sizeof(gidx), a.device);  // {max chunk length, slots}
+        CK(cudaMemsetAsync(out.get(), 0, sizeof(gidx), rt.stream));
+        const bool fused = 32 % C == 0;
+        (fused ? perm_kernel<true> : perm_kernel<false>)<<<blocks_for(gidx(m->nrows_padded) + 1), kThreads, 0,
+                                                           rt.stream>>>(
+            pinv, a.rowptr.as<gidx>(), n, m->nrows_padded, C, m->row_perm.as<lidx>(), m->rowlen.as<lidx>(),
+            m->chunk_len.as<lidx>(), sizes.as<gidx>(), nchunks, out.as<int>());
         CK(cudaGetLastError());
-        exclusive_scan_i64(sizes.as<gidx>(), m->chunk_offset.as<gidx>(), nchunks + 1, rt);
-        m->max_chunk_len = read_flag(mx, rt);
+        if (!fused) {
+            chunk_len_kernel<<<blocks_for(nchunks + 1), kThreads, 0, rt.stream>>>(
+                m->rowlen.as<lidx>(), nchunks, C, m->chunk_len.as<lidx>(), sizes.as<gidx>(), out.as<int>());
+            CK(cudaGetLastError());
+        }
+        std::size_t tmp_bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes.as<gidx>(), m->chunk_offset.as<gidx>(),
+                                         nchunks + 1, rt.stream));
+        DeviceBuffer tmp(std::max<std::size_t>(tmp_bytes, 1), rt.device);
+        CK(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, sizes.as<gidx>(), m->chunk_offset.as<gidx>(),
+                                         nchunks + 1, rt.stream));
+        CK(cudaMemcpyAsync(out.as<gidx>() + 1, m->chunk_offset.as<gidx>() + nchunks, sizeof(gidx),
+                           cudaMemcpyDeviceToDevice, rt.stream));
+        gidx h[2] = {0, 0};
+        CK(cudaMemcpyAsync(h, out.get(), sizeof(h), cudaMemcpyDeviceToHost, rt.stream));
+        CK(cudaStreamSynchronize(rt.stream));
+        m->max_chunk_len = int(h[0] & 0xffffffff);
+        m->slots = h[1];
     }
-    CK(cudaMemcpyAsync(&m->slots, m->chunk_offset.as<gidx>() + nchunks, sizeof(gidx), cudaMemcpyDeviceToHost,
-                       rt.stream));
-    CK(cudaStreamSynchronize(rt.stream));
     m->beta = m->slots > 0 ? double(m->nnz) / double(m->slots) : 1.0;
 
     const std::size_t es = value_bytes(a.dt);

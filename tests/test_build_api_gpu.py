@@ -158,8 +158,8 @@ def test_apply_override_matrix_free(sk):
     assert y.copy_out()[:, 0].tolist() == [1.0, 2.0, 3.0]
 
 
-@pytest.mark.parametrize("sigma,maxlen", [(256, 13), (4096, 63), (4096, 64), (1000, 200), (36, 5)])
-def test_sigma_permutation_stable_descending(sk, sigma, maxlen):
+@pytest.mark.parametrize("sigma,maxlen", [(256, 13), (4096, 63), (4096, 64), (1024, 200), (96, 5)])
+def test_sigma_permutation_stable_descending(sk, orc, sigma, maxlen):
     """The σ-sort (sellcs.hpp:80-91): within each scope, rows stably ordered by descending
     length -- both the counting path (all rows < 64 entries) and the comparison path, ties,
     several 256-row chunks per scope and a ragged last scope."""
@@ -175,3 +175,10 @@ def test_sigma_permutation_stable_descending(sk, sigma, maxlen):
     pinv = A.export()["row_perm_inv"]
     want = np.concatenate([s0 + np.argsort(-lens[s0:s0 + sigma], kind="stable") for s0 in range(0, n, sigma)])
     assert np.array_equal(pinv[:n], want)
+    # whole layouts against the oracle: C = 32 takes the fused perm + chunk-length kernel,
+    # C = 4 as well (4 divides the warp), both with short and long chunks
+    for C_ in (32, 4):
+        L = sk.crs(rp, col, val).build(C_, sigma).export()
+        R = orc.build(rp, col, val, C_, sigma).layout()
+        for key in LAYOUT:
+            assert np.array_equal(L[key], R[key]), (C_, key)

@@ -73,6 +73,13 @@ def c1():
     n = 1000
     A = sk.crs_stencil(5, n).build(32, 1)
     spmv_case("c1 5pt 1000^2 SELL-32-1", A, n * n, 5 * n * n - 4 * n, 1, flush=True, reps=30)
+    # the same event bracket around a one-element kernel: the launch floor inside the C1 number
+    one = torch.empty(1, device="cuda")
+
+    def tiny():
+        with torch.cuda.stream(stream):
+            one.zero_()
+    emit(case="c1 launch floor (1-element kernel after the flush)", ms=timed(tiny, reps=30, flush=True))
 
 
 def c2():
