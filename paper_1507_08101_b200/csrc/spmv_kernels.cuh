@@ -920,20 +920,11 @@ constexpr std::size_t rows_stage_bytes() {
     constexpr int S = RGeom<T, W, DOTS>::STAGES;
     return (std::size_t(S) * RGeom<T, W>::SB + std::size_t(S) * sizeof(StageHdr) + 2 * S * 8 + 15) / 16 * 16;
 }
-// SK_YBULK: the epilogue-free kernel of the wide plans writes y through shared memory
-// and one bulk store per warp pass (two 1-KB buffers per consumer warp) instead of STG
-#ifndef SK_YBULK
-#define SK_YBULK 0
-#endif
-template <class T, int W, bool PLAIN>
-constexpr bool rows_ybulk() {
-    return SK_YBULK && PLAIN && RGeom<T, W>::WIDE && RPlan<T, W>::VEC * sizeof(T) == 32;
-}
-template <class T, int W, bool DOTS, bool PLAIN = false>
+template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
     return rows_stage_bytes<T, W, DOTS>() +
            (DOTS && !dots_in_registers<T, W>() ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) +
-           (rows_ybulk<T, W, PLAIN>() ? std::size_t(kNCW) * 2 * 1024 : 0) + 128;
+           128;
 }
 
 // DYN: the kernel can take its tiles from a.tile_counter (dynamic deal); a separate
@@ -1092,9 +1083,6 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
         // slots (no 3 x VEC accumulators live across the gather loop); the lanes are
         // reduced once at the end, in a fixed order (deterministic)
         T* dacc = reinterpret_cast<T*>(smem + rows_stage_bytes<T, W, DOTS>());
-        char* ystage = reinterpret_cast<char*>(smem + rows_stage_bytes<T, W, DOTS>());  // PLAIN: no dot slots
-        const bool ybulk = rows_ybulk<T, W, PLAIN>() && a.y_rs == W;  // compact y: a pass's rows are contiguous
-        int ypass = 0;
         const int cl = warp * 32 + lane;  // consumer lane
         constexpr int NCL = kNCW * 32;
         constexpr bool kDR = dots_in_registers<T, W>();
@@ -1252,37 +1240,7 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
                 gather(a.val + h.off0, a.col + h.off0);
             if constexpr (PLAIN) {
                 // y = A x with alpha == 1 and no other flag: t * 1 == t, so the store is the result
-#ifndef SK_DEBUG_NOSTORE
-#define SK_DEBUG_NOSTORE 0
-#endif
-                // SK_DEBUG_NOSTORE (experiments only): keep the sweep, drop the y stores
-                if constexpr (rows_ybulk<T, W, PLAIN>()) {
-                    if (ybulk) {
-                        // the bulk store that last read this buffer (two passes ago) is done
-                        char* buf = ystage + (warp * 2 + (ypass & 1)) * 1024;
-                        if (lane == 0) bulk_wait_read<1>();
-                        __syncwarp();
-                        if (row < row_end) {
-                            Vec<T, VEC> out;
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) out.v[e] = acc[e];
-                            *reinterpret_cast<Vec<T, VEC>*>(buf + lane * 32) = out;  // = (rl * W + sub * VEC) * 8
-                        }
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            const int r0 = tile_row0 + wrow0;
-                            const int nv = min(WR, row_end - r0);
-                            if (nv > 0)
-                                bulk_s2g(a.y + (unsigned long long)unsigned(r0) * W, buf,
-                                         std::uint32_t(nv) * W * std::uint32_t(sizeof(T)));
-                            bulk_commit();  // (an empty group when nothing was stored: the count stays per pass)
-                        }
-                        ++ypass;
-                        continue;
-                    }
-                }
-                if (row < row_end && (!SK_DEBUG_NOSTORE || *reinterpret_cast<const unsigned*>(&acc[0]) == 0x7fc0deadu)) {
+                if (row < row_end) {
                     Vec<T, VEC> out;
 #pragma unroll
                     for (int e = 0; e < VEC; ++e) out.v[e] = acc[e];
@@ -1356,9 +1314,6 @@ __global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double>
             }  // pass
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);  // matrix data of the tile consumed
-        }
-        if constexpr (rows_ybulk<T, W, PLAIN>()) {
-            if (lane == 0) bulk_wait_all();  // the y stores complete before the CTA (and its shared memory) ends
         }
         if constexpr (DOTS && kDirect) {
             // lanes of a row slot -> warp total per column (fixed butterfly order)
@@ -1606,7 +1561,7 @@ LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cu
     if (!DYN) a.tile_counter = nullptr;
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED, DYN>;
-    constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS, PLAIN>();
+    constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
     static std::atomic<std::uint64_t> attr_devs{0};
     smem_attr_per_device(kern, smem, rt.device, attr_devs);
     static int per_sm = [&] {
@@ -1651,11 +1606,6 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
             const bool dots = (a.flags & kFlagDots) != 0;
             int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
                                cap);
-            static const int rgt_env = [] {  // A/B knob: row groups per tile
-                const char* e = std::getenv("SELLKIT_RTILE_GROUPS");
-                return e ? std::max(1, std::atoi(e)) : 0;
-            }();
-            if (rgt_env > 0) rgt = std::min(rgt_env, cap);
             while (a.sweep_brg > 0 && rgt > 1 && a.sweep_brg % rgt != 0) --rgt;  // tiles inside blocks
             if (rgt >= 1 && a.row_map != nullptr)  // remote-part sweep of a distributed matrix
                 return dots ? launch_tma_rows<T, C, W, true, false, true>(a, rgt, rt, st)

@@ -50,21 +50,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32
 }
 
 // Bulk L2 prefetch of a global range (size multiple of 16, 16-B aligned).
-// shared -> global bulk store (bulk-group completion), its group bookkeeping, and the
-// generic -> async proxy fence a thread issues after writing what such a store reads
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, std::uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, std::uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
