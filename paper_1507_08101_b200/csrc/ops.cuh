@@ -155,6 +155,14 @@ __device__ __forceinline__ Vec<T, N> ld_x(const T* p) {
         using R = typename RawVec<B>::type;
         R raw = __ldg(reinterpret_cast<const R*>(p));
         memcpy(&r, &raw, B);
+    } else if constexpr (B % 32 == 0) {  // 64-/128-byte lane vectors: consecutive 32-byte loads
+        constexpr int M = 32 / int(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < N / M; ++q) {
+            const Vec<T, M> h = ld_x<T, M>(p + q * M);
+#pragma unroll
+            for (int i = 0; i < M; ++i) r.v[q * M + i] = h.v[i];
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) r.v[i] = p[i];
@@ -177,6 +185,14 @@ __device__ __forceinline__ Vec<T, N> ld_vec(const T* p) {
         using R = typename RawVec<B>::type;
         R raw = *reinterpret_cast<const R*>(p);
         memcpy(&r, &raw, B);
+    } else if constexpr (B % 32 == 0) {
+        constexpr int M = 32 / int(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < N / M; ++q) {
+            const Vec<T, M> h = ld_vec<T, M>(p + q * M);
+#pragma unroll
+            for (int i = 0; i < M; ++i) r.v[q * M + i] = h.v[i];
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) r.v[i] = p[i];
@@ -197,6 +213,15 @@ __device__ __forceinline__ void st_vec(T* p, const Vec<T, N>& v) {
         R raw;
         memcpy(&raw, &v, B);
         *reinterpret_cast<R*>(p) = raw;
+    } else if constexpr (B % 32 == 0) {
+        constexpr int M = 32 / int(sizeof(T));
+#pragma unroll
+        for (int q = 0; q < N / M; ++q) {
+            Vec<T, M> h;
+#pragma unroll
+            for (int i = 0; i < M; ++i) h.v[i] = v.v[q * M + i];
+            st_vec<T, M>(p + q * M, h);
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < N; ++i) p[i] = v.v[i];

@@ -350,6 +350,9 @@ __global__ void __launch_bounds__(kBlock) spmv_cw_kernel(const KArgs<T> a) {
 #ifndef SK_MINB
 #define SK_MINB 2
 #endif
+#ifndef SK_MINB_WIDE  // CTAs/SM of the column-slice kernel for complex-double RHS rows of 512 B and more
+#define SK_MINB_WIDE 1  // (2 spills 176-520 B: cplx w = 32 / 64 plain 22.8 / 41.3 -> 19.3 / 32.1 ms, r2bd)
+#endif
 constexpr int kNCW = SK_NCW;
 constexpr int kTmaThreads = (kNCW + 1) * 32;
 constexpr int kStageBytes = SK_STAGE_KB * 1024;
@@ -478,7 +481,8 @@ __device__ __forceinline__ void tma_rowgroup(const KArgs<T>& a, const T* sval, c
 }
 
 template <class T, int C, int W, int U>
-__global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
+__global__ void __launch_bounds__(kTmaThreads, sizeof(T) >= 16 && sizeof(T) * W >= 512 ? SK_MINB_WIDE : SK_MINB)
+    spmv_tma_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     // tile of this CTA's it-th iteration: segments of `seg` consecutive tiles dealt
     // round-robin over the CTAs (seg = 1: plain round-robin)
     auto tile_of = [&](int it, int sg) -> gidx {
@@ -683,6 +687,9 @@ __global__ void __launch_bounds__(kTmaThreads, SK_MINB) spmv_tma_kernel(const KA
 #ifndef SK_RVEC
 #define SK_RVEC 32  // bytes of one RHS row a lane gathers per nonzero
 #endif
+#ifndef SK_ROWS_WIDE  // 1: the rows kernel also for RHS rows of 512 B / 1 KB (else the column-slice kernel)
+#define SK_ROWS_WIDE 1
+#endif
 #ifndef SK_PREFETCH_EPI
 #define SK_PREFETCH_EPI 1
 #endif
@@ -694,7 +701,10 @@ template <class T, int W>
 struct RPlan {
     static constexpr int E = int(sizeof(T));
     static constexpr int VB = SK_RVEC / E > 0 ? SK_RVEC / E : 1;
-    static constexpr int VEC = VB < W ? VB : W;
+    // RHS rows wider than 8 lanes x 32 B (512-B / 1-KB rows): 64- or 128-byte lane vectors
+    // (2 or 4 LDG.256 per gather), still 8 lanes per row
+    static constexpr int VW = (SK_ROWS_WIDE && W * E > 8 * SK_RVEC && W % 8 == 0) ? W / 8 : VB;
+    static constexpr int VEC = VW < W ? VW : W;
     static constexpr int TPR = W / VEC;   // lanes per row
     static constexpr int WR = 32 / TPR;   // rows per warp
     static constexpr bool ok = TPR >= 1 && TPR <= 8 && W % VEC == 0 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0;
@@ -927,12 +937,21 @@ constexpr std::size_t rows_smem_bytes() {
            128;
 }
 
+// CTAs/SM the rows kernel is compiled for (register budget 65536 / (288 x this));
+// the 64-/128-byte lane vectors of the wide plans need 2 / 1
+template <class T, int W, bool DOTS>
+constexpr int rows_minb() {
+    constexpr int vb = RPlan<T, W>::VEC * int(sizeof(T));
+    if constexpr (vb > 64) return 1;
+    else if constexpr (vb > SK_RVEC) return 2;
+    else if constexpr (DOTS) return std::is_same_v<T, double> && W == 1 ? SK_RMINB_DOTS_NARROW : SK_RMINB_DOTS;
+    else return SK_RMINB;
+}
+
 // DYN: the kernel can take its tiles from a.tile_counter (dynamic deal); a separate
 // instantiation so the static epilogue-free kernel keeps its register schedule.
 template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED, bool DYN>
-__global__ void __launch_bounds__(kTmaThreads, DOTS ? (std::is_same_v<T, double> && W == 1 ? SK_RMINB_DOTS_NARROW
-                                                                                         : SK_RMINB_DOTS)
-                                                    : SK_RMINB)
+__global__ void __launch_bounds__(kTmaThreads, rows_minb<T, W, DOTS>())
     spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
     using P = RPlan<T, W>;

@@ -788,10 +788,20 @@ void tsmttsm(DenseMat& x, const DenseMat& v_in, const DenseMat& w_in, const void
                     }
                     return 0;
                 }
-                if (m <= 8 && k <= 8) {
+                // the Kahan register kernel keeps sum + compensation of every cell: an 8 x 8
+                // block would not fit the register file (1.1 KB of spills), so it takes the
+                // shared-memory tile kernel below
+                const bool kahan_regs_ok = !kahan || p2(m) * p2(k) <= 32;
+                if (m <= 8 && k <= 8 && kahan_regs_ok) {
                     auto go = [&]<int MM, int KK>() {
-                        if (kahan) tsmttsm_reg_kernel<T, MM, KK, true><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
-                        else tsmttsm_reg_kernel<T, MM, KK, false><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
+                        if constexpr (MM * KK <= 32) {
+                            if (kahan) {
+                                tsmttsm_reg_kernel<T, MM, KK, true><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k,
+                                                                                                 rows_per, p, pc);
+                                return;
+                            }
+                        }
+                        tsmttsm_reg_kernel<T, MM, KK, false><<<nparts, kT, 0, rt.stream>>>(vp, vst, wp, wst, n, m, k, rows_per, p, pc);
                     };
                     auto gok = [&]<int MM>() {
                         switch (p2(k)) {

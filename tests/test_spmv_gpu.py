@@ -154,6 +154,42 @@ def test_complex_vs_oracle(sk, orc):
         assert np.allclose(dots, do, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("dt,w", [("r64", 64), ("c64", 32), ("c64", 64), ("r32", 64), ("c32", 64)])
+@pytest.mark.parametrize("C,sigma", [(32, 256), (8, 32), (4, 1)])
+def test_wide_rhs_rows(sk, orc, dt, w, C, sigma):
+    """RHS rows of 512 B / 1 KB (the rows kernel with 64- / 128-byte lane vectors): y
+    bit-identical to the oracle for the plain sweep and the KPM step, dots within 1e-12."""
+    rng = np.random.default_rng(w + C)
+    cplx = dt in ("c64", "c32")
+    rp, c, v = random_crs(rng, 700, 700, 0.012, cplx=cplx)
+    sdt = {"r64": sellkit.R64, "c64": sellkit.C64, "r32": sellkit.R32, "c32": sellkit.C32}[dt]
+    npdt = sellkit.NP_DTYPE[sdt]
+    v = v.astype(npdt)
+    A = sk.crs(rp, c, v, dt=sdt).build(C, sigma)
+    Ao = orc.build(rp, c, v.astype(np.complex128 if cplx else np.float64), C, sigma)
+    xv = rng.uniform(-1, 1, (700, w)) + (1j * rng.uniform(-1, 1, (700, w)) if cplx else 0)
+    y0 = rng.uniform(-1, 1, (700, w)) + (1j * rng.uniform(-1, 1, (700, w)) if cplx else 0)
+    xv, y0 = xv.astype(npdt), y0.astype(npdt)
+    x = sk.densemat_from(xv)
+    y = sk.densemat(700, w, sdt)
+    sk.spmv(y, A, x)
+    if dt in ("r64", "c64"):
+        yo, _, _ = orc.spmv(Ao, xv)
+        assert np.array_equal(y.copy_out(), yo)
+        y = sk.densemat_from(y0)
+        dots = np.zeros(3 * w, npdt)
+        flags = sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX
+        al = 0.5 + 0.25j if cplx else 0.5
+        ga = 0.1 - 0.2j if cplx else 0.25
+        sk.spmv(y, A, x, flags=flags, alpha=al, beta=-1.0, gamma=ga, dot=dots)
+        yo, _, do = orc.spmv(Ao, xv, y0, None, flags, alpha=al, beta=-1.0, gamma=ga)
+        assert np.array_equal(y.copy_out(), yo)
+        assert np.allclose(dots, do, rtol=1e-12, atol=1e-12)
+    else:  # single precision: against the oracle's double-precision sweep of the same values
+        yo, _, _ = orc.spmv(Ao, xv.astype(np.complex128 if cplx else np.float64))
+        assert np.max(np.abs(y.copy_out() - yo)) <= 1e-4 * (1 + np.max(np.abs(yo)))
+
+
 def test_ti_generator_and_kpm_step(sk, orc):
     """C3: the device TI Hamiltonian equals the numpy restatement; the augmented KPM
     step y = 2a(H - bI)x - y with <y,y>, <x,y>, <x,x> (w = 16, complex) is bit-identical
@@ -341,7 +377,7 @@ def test_large_stencil_bitwise(sk, orc):
     assert dots_close(dots, do, sc)
 
 
-@pytest.mark.parametrize("w", [1, 4, 8, 16, 32])
+@pytest.mark.parametrize("w", [1, 4, 8, 16, 32, 64])
 @pytest.mark.parametrize("C,sigma", [(32, 256), (8, 64), (4, 1)])
 def test_irregular_rows_all_paths(sk, orc, w, C, sigma):
     """Rows of very different lengths (empty rows, a 3000-nonzero row, a dense block of

@@ -88,6 +88,22 @@ def test_kahan_cancellation(sk):
     assert run_tsmttsm(sk, v, w, np.zeros((1, 1)), 1.0, 0.0, kahan=True)[0, 0] == 1.0
 
 
+@pytest.mark.parametrize("m,k", [(1, 1), (2, 4), (4, 4), (4, 8), (8, 8), (3, 7), (16, 16)])
+def test_kahan_shapes(sk, orc, m, k):
+    """Kahan TSMTTSM on every kernel it routes to (register kernel up to 32 cells, the
+    shared-memory tile kernel for 8 x 8 and wider): the cancellation KAT in every cell, and
+    random data against the oracle's compensated sums."""
+    v = np.ones((3, m))
+    w = np.tile(np.array([[1e16], [1.0], [-1e16]]), (1, k))
+    assert np.array_equal(run_tsmttsm(sk, v, w, np.zeros((m, k)), 1.0, 0.0, kahan=True), np.ones((m, k)))
+    rng = np.random.default_rng(m * 31 + k)
+    n = 5000
+    V, W, X = rng.uniform(-1, 1, (n, m)), rng.uniform(-1, 1, (n, k)), rng.uniform(-1, 1, (m, k))
+    want = orc.tsmttsm(V, W, X, 0.75, 0.5, kahan=True)
+    got = run_tsmttsm(sk, V, W, X, 0.75, 0.5, kahan=True)
+    assert np.all(np.abs(got - want) <= 1e-12 * (1 + np.abs(V).T @ np.abs(W) + np.abs(X)))
+
+
 def test_tsmm_inplace_and_gemm(sk, orc):
     rng = np.random.default_rng(8)
     n, m = 700, 6

@@ -26,12 +26,13 @@ p.add_argument("--order", default="rows")
 p.add_argument("--reps", type=int, default=20)
 p.add_argument("--warm", type=int, default=3)
 p.add_argument("--flags", default="kpm", choices=["kpm", "plain", "axpby"])
+p.add_argument("--w", type=int, default=16)
 a = p.parse_args()
 
 sk = sellkit.load()
 stream = torch.cuda.ExternalStream(sk.stream())
 PEAK = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
-lx, ly, lz, w = 256, 128, 128, 16
+lx, ly, lz, w = 256, 128, 128, a.w
 N = 4 * lx * ly * lz
 dt = sellkit.C64 if a.dt == "c64" else sellkit.R64
 vb = 16 if dt == sellkit.C64 else 8
@@ -83,6 +84,6 @@ ms = float(np.median(ts))
 nvec = 2 + (1 if flags & sellkit.AXPBY else 0)
 alg = (vb + 4.0) * nnz + vb * w * N * nvec
 fl = (8.0 if dt == sellkit.C64 else 2.0) * nnz * w
-print(json.dumps({"case": f"c3 TI 2^24 rows w=16 {a.dt} {a.flags}", "order": a.order, "ms": ms, "min_ms": min(ts),
+print(json.dumps({"case": f"c3 TI 2^24 rows w={w} {a.dt} {a.flags}", "order": a.order, "ms": ms, "min_ms": min(ts),
                   "gflops": fl / ms / 1e6, "gbs": alg / ms / 1e6, "frac": alg / ms / 1e6 / PEAK, "nnz": nnz}),
       flush=True)
