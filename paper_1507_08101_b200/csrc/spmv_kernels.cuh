@@ -690,6 +690,9 @@ __global__ void __launch_bounds__(kTmaThreads, sizeof(T) >= 16 && sizeof(T) * W 
 #ifndef SK_ROWS_WIDE  // 1: the rows kernel also for RHS rows of 512 B / 1 KB (else the column-slice kernel)
 #define SK_ROWS_WIDE 1
 #endif
+#ifndef SK_WIDE_LANES  // lanes per RHS row of 512 B / 1 KB; 0: by kernel variant (rows_lanes)
+#define SK_WIDE_LANES 0
+#endif
 #ifndef SK_PREFETCH_EPI
 #define SK_PREFETCH_EPI 1
 #endif
@@ -697,18 +700,35 @@ constexpr bool kPrefetchEpi = SK_PREFETCH_EPI != 0;
 constexpr bool kXHint = SK_XPOL != 0;  // x gathers marked evict_last in L2
 constexpr bool kYHint = SK_YPOL != 0;  // y / z stores marked evict_first in L2
 
-template <class T, int W>
+// Lanes per RHS row of 512 B / 1 KB (measured, r2bi): the dots kernels take 8 (64- / 128-byte
+// lane vectors; their tile is one pass of 32 rows); the others 16 for real rows and 1-KB
+// rows (double w = 64 plain 7.77 -> 5.77 ms, complex w = 64 29.9 -> 16.6 ms), 8 for
+// complex w = 32 (plain 8.0 vs 8.8 ms)
+template <class T, int W, bool DOTS>
+constexpr int rows_lanes() {
+    if constexpr (SK_WIDE_LANES > 0) return SK_WIDE_LANES;
+    else if constexpr (DOTS) return 8;
+    else return (sizeof(T) <= 8 || W * int(sizeof(T)) >= 1024) ? 16 : 8;
+}
+
+template <class T, int W, int WL = 8>
 struct RPlan {
     static constexpr int E = int(sizeof(T));
     static constexpr int VB = SK_RVEC / E > 0 ? SK_RVEC / E : 1;
     // RHS rows wider than 8 lanes x 32 B (512-B / 1-KB rows): 64- or 128-byte lane vectors
     // (2 or 4 LDG.256 per gather), still 8 lanes per row
-    static constexpr int VW = (SK_ROWS_WIDE && W * E > 8 * SK_RVEC && W % 8 == 0) ? W / 8 : VB;
+    // (WL = 16 / 32 lanes per wide row: 8 / 16 rows per pass)
+    static constexpr bool WIDE_ROW = SK_ROWS_WIDE && W * E > 8 * SK_RVEC && W % WL == 0;
+    static constexpr int VW = WIDE_ROW ? (W * E / WL >= SK_RVEC ? W / WL : VB) : VB;
     static constexpr int VEC = VW < W ? VW : W;
     static constexpr int TPR = W / VEC;   // lanes per row
     static constexpr int WR = 32 / TPR;   // rows per warp
-    static constexpr bool ok = TPR >= 1 && TPR <= 8 && W % VEC == 0 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0;
+    static constexpr bool ok = TPR >= 1 && W % VEC == 0 &&
+                               ((TPR <= 8 && kNCW * WR >= 32 && (kNCW * WR) % 32 == 0) ||
+                                (WIDE_ROW && TPR <= 32 && 32 % (kNCW * WR) == 0));
 };
+template <class T, int W, bool DOTS>
+using RP = RPlan<T, W, rows_lanes<T, W, DOTS>()>;
 
 // Per-lane shared-memory dot slot += v.  Only the owning lane touches a slot, so the
 // order of additions is fixed.  (A shared-memory atomicAdd on doubles compiles to a
@@ -916,7 +936,7 @@ __device__ __forceinline__ void tail_dispatch(int r, F& f) {
 
 template <class T, int W, bool DOTS = false>
 struct RGeom {
-    static constexpr bool WIDE = RPlan<T, W>::TPR > 1;
+    static constexpr bool WIDE = RPlan<T, W>::TPR > 1;  // (the same for every lane count)
     static constexpr int STAGES =
         (DOTS && SK_RSTAGES_DOTS > 0) ? SK_RSTAGES_DOTS : (WIDE ? SK_RSTAGES_WIDE : SK_RSTAGES_NARROW);
     static constexpr int SB = (WIDE ? SK_RSTAGE_KB : SK_RSTAGE_KB_NARROW) * 1024;
@@ -933,7 +953,7 @@ constexpr std::size_t rows_stage_bytes() {
 template <class T, int W, bool DOTS>
 constexpr std::size_t rows_smem_bytes() {
     return rows_stage_bytes<T, W, DOTS>() +
-           (DOTS && !dots_in_registers<T, W>() ? std::size_t(3) * RPlan<T, W>::VEC * kNCW * 32 * sizeof(T) : 0) +
+           (DOTS && !dots_in_registers<T, W>() ? std::size_t(3) * RP<T, W, true>::VEC * kNCW * 32 * sizeof(T) : 0) +
            128;
 }
 
@@ -941,7 +961,7 @@ constexpr std::size_t rows_smem_bytes() {
 // the 64-/128-byte lane vectors of the wide plans need 2 / 1
 template <class T, int W, bool DOTS>
 constexpr int rows_minb() {
-    constexpr int vb = RPlan<T, W>::VEC * int(sizeof(T));
+    constexpr int vb = RP<T, W, DOTS>::VEC * int(sizeof(T));
     if constexpr (vb > 64) return 1;
     else if constexpr (vb > SK_RVEC) return 2;
     else if constexpr (DOTS) return std::is_same_v<T, double> && W == 1 ? SK_RMINB_DOTS_NARROW : SK_RMINB_DOTS;
@@ -954,7 +974,7 @@ template <class T, int C, int W, int U, bool DOTS, bool PLAIN, bool MAPPED, bool
 __global__ void __launch_bounds__(kTmaThreads, rows_minb<T, W, DOTS>())
     spmv_tma_rows_kernel(const KArgs<T> a, int rgt, gidx ntiles, int seg) {
     using O = Ops<T>;
-    using P = RPlan<T, W>;
+    using P = RP<T, W, DOTS>;
     constexpr int VEC = P::VEC, TPR = P::TPR, WR = P::WR;
     constexpr int SCAP = RGeom<T, W>::SCAP;
     constexpr int SB = RGeom<T, W>::SB;
@@ -1557,7 +1577,7 @@ LaunchShape launch_tma(const KArgs<T>& a, int rgt, DeviceRuntime& rt, cudaStream
 // target (SK_RMINB CTAs/SM: 56 registers per thread at 4).
 template <class T, int W, bool DOTS>
 constexpr int rows_unroll() {
-    constexpr int per = RPlan<T, W>::VEC * int(sizeof(T)) / 4 + int(sizeof(T)) / 4 + 1;
+    constexpr int per = RP<T, W, DOTS>::VEC * int(sizeof(T)) / 4 + int(sizeof(T)) / 4 + 1;
     constexpr int budget = DOTS ? SK_RUBUDGET_DOTS : SK_RUBUDGET;
     constexpr int u = budget / per;
     return u < 1 ? 1 : (u > 8 ? 8 : u);
@@ -1614,7 +1634,7 @@ template <class T, int C, int W>
 LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lidx max_chunk_len) {
     using P = Plan<T, W>;
     constexpr int U = unroll_of<T, P>();
-    if constexpr (RPlan<T, W>::ok) {
+    if constexpr (RP<T, W, false>::ok && RP<T, W, true>::ok) {
         const int rm = rows_mode();
         const bool rows = rm != 0;
         const bool stride_ok = gidx(a.x_rs) * gidx(sizeof(T)) < (gidx(1) << 31);  // 32-bit byte stride
@@ -1623,7 +1643,7 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
             // rows are few), as far as one stage holds them
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
             const bool dots = (a.flags & kFlagDots) != 0;
-            int rgt = std::min((dots ? kNCW * RPlan<T, W>::WR : std::max(kNCW * RPlan<T, W>::WR, SK_RTILE_ROWS)) / 32,
+            int rgt = std::min((dots ? kNCW * RP<T, W, true>::WR : std::max(kNCW * RP<T, W, false>::WR, SK_RTILE_ROWS)) / 32,
                                cap);
             while (a.sweep_brg > 0 && rgt > 1 && a.sweep_brg % rgt != 0) --rgt;  // tiles inside blocks
             if (rgt >= 1 && a.row_map != nullptr)  // remote-part sweep of a distributed matrix
