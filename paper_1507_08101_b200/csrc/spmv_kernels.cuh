@@ -693,6 +693,9 @@ __global__ void __launch_bounds__(kTmaThreads, sizeof(T) >= 16 && sizeof(T) * W 
 #ifndef SK_WIDE_LANES  // lanes per RHS row of 512 B / 1 KB; 0: by kernel variant (rows_lanes)
 #define SK_WIDE_LANES 0
 #endif
+#ifndef SK_WIDE_DOTS_LANES  // the same for the dots kernels: 16, two 16-row passes per 32-row tile
+#define SK_WIDE_DOTS_LANES 16  // (KPM, TI 2^24 rows, r2bl: complex w = 32 / 64 12.7 / 39.4 -> 11.4 / 27.9 ms,
+#endif                         //  double w = 64 10.9 -> 9.8 ms against 8 lanes of 64- / 128-byte vectors)
 #ifndef SK_PREFETCH_EPI
 #define SK_PREFETCH_EPI 1
 #endif
@@ -700,14 +703,14 @@ constexpr bool kPrefetchEpi = SK_PREFETCH_EPI != 0;
 constexpr bool kXHint = SK_XPOL != 0;  // x gathers marked evict_last in L2
 constexpr bool kYHint = SK_YPOL != 0;  // y / z stores marked evict_first in L2
 
-// Lanes per RHS row of 512 B / 1 KB (measured, r2bi): the dots kernels take 8 (64- / 128-byte
-// lane vectors; their tile is one pass of 32 rows); the others 16 for real rows and 1-KB
-// rows (double w = 64 plain 7.77 -> 5.77 ms, complex w = 64 29.9 -> 16.6 ms), 8 for
-// complex w = 32 (plain 8.0 vs 8.8 ms)
+// Lanes per RHS row of 512 B / 1 KB (measured, r2bi / r2bl): the dots kernels 16 (two passes
+// per 32-row tile); the others 16 for real rows and 1-KB rows (double w = 64 plain 7.77 ->
+// 5.77 ms, complex w = 64 29.9 -> 16.6 ms), 8 (64-byte lane vectors) for complex w = 32
+// (plain 8.0 vs 8.8 ms)
 template <class T, int W, bool DOTS>
 constexpr int rows_lanes() {
     if constexpr (SK_WIDE_LANES > 0) return SK_WIDE_LANES;
-    else if constexpr (DOTS) return 8;
+    else if constexpr (DOTS) return SK_WIDE_DOTS_LANES;
     else return (sizeof(T) <= 8 || W * int(sizeof(T)) >= 1024) ? 16 : 8;
 }
 
@@ -1148,7 +1151,8 @@ __global__ void __launch_bounds__(kTmaThreads, rows_minb<T, W, DOTS>())
         const int row_end = int(min(gidx(a.nrows), a.rg1 * 32));          // rows stored
         // (compile-time bound: one pass for the dots variant, whose register budget
         // has no room for the pass loop -- measured 30 % slower on C3 C64)
-        constexpr int kMaxPasses = DOTS ? 1 : (SK_RTILE_ROWS / (kNCW * WR) > 1 ? SK_RTILE_ROWS / (kNCW * WR) : 1);
+        constexpr int kMaxPasses = DOTS ? (kNCW * WR < 32 ? 32 / (kNCW * WR) : 1)
+                                        : (SK_RTILE_ROWS / (kNCW * WR) > 1 ? SK_RTILE_ROWS / (kNCW * WR) : 1);
         const int passes = min(kMaxPasses, (rows_per_tile + kNCW * WR - 1) / (kNCW * WR));
         for (int it = 0;; ++it) {
             if (!dyn) {
@@ -1643,7 +1647,8 @@ LaunchShape launch_cw(const KArgs<T>& a, DeviceRuntime& rt, cudaStream_t st, lid
             // rows are few), as far as one stage holds them
             const int cap = RGeom<T, W>::SCAP / (32 * std::max<lidx>(1, max_chunk_len));
             const bool dots = (a.flags & kFlagDots) != 0;
-            int rgt = std::min((dots ? kNCW * RP<T, W, true>::WR : std::max(kNCW * RP<T, W, false>::WR, SK_RTILE_ROWS)) / 32,
+            int rgt = std::min((dots ? std::max(kNCW * RP<T, W, true>::WR, 32)
+                                     : std::max(kNCW * RP<T, W, false>::WR, SK_RTILE_ROWS)) / 32,
                                cap);
             while (a.sweep_brg > 0 && rgt > 1 && a.sweep_brg % rgt != 0) --rgt;  // tiles inside blocks
             if (rgt >= 1 && a.row_map != nullptr)  // remote-part sweep of a distributed matrix
