@@ -190,6 +190,35 @@ def test_wide_rhs_rows(sk, orc, dt, w, C, sigma):
         assert np.max(np.abs(y.copy_out() - yo)) <= 1e-4 * (1 + np.max(np.abs(yo)))
 
 
+@pytest.mark.parametrize("off", [0, 8, 1])
+def test_wide_column_views(sk, orc, off):
+    """64-column row-major views into 80-column parents (sellkit_densemat_view with a
+    contiguous column range): strided x and y rows, 64-B aligned (off 0, 8) and not (off 1,
+    which must leave the vector kernels); y bit-identical to the oracle, other columns untouched."""
+    import ctypes as C
+    rng = np.random.default_rng(11 + off)
+    rp, c, v = random_crs(rng, 600, 600, 0.015)
+    A = sk.crs(rp, c, v).build(32, 64)
+    Ao = orc.build(rp, c, v, 32, 64)
+    X = rng.uniform(-1, 1, (600, 80))
+    Y = rng.uniform(-1, 1, (600, 80))
+    xp, yp = sk.densemat_from(X), sk.densemat_from(Y)
+    cols = (C.c_int32 * 64)(*range(off, off + 64))
+    xh, yh = C.c_void_p(), C.c_void_p()
+    sk.call("sellkit_densemat_view", xp.h, 0, 600, cols, 64, C.byref(xh))
+    sk.call("sellkit_densemat_view", yp.h, 0, 600, cols, 64, C.byref(yh))
+    x, y = sellkit.DenseMat(sk, xh, sellkit.R64), sellkit.DenseMat(sk, yh, sellkit.R64)
+    flags = sellkit.AXPBY | sellkit.SHIFT
+    sk.spmv(y, A, x, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    yo, _, _ = orc.spmv(Ao, np.ascontiguousarray(X[:, off:off + 64]), np.ascontiguousarray(Y[:, off:off + 64]), None,
+                        flags, alpha=0.5, beta=-1.0, gamma=0.25)
+    got = yp.copy_out()
+    assert np.array_equal(got[:, off:off + 64], yo)
+    rest = np.ones(80, bool)
+    rest[off:off + 64] = False
+    assert np.array_equal(got[:, rest], Y[:, rest])
+
+
 def test_ti_generator_and_kpm_step(sk, orc):
     """C3: the device TI Hamiltonian equals the numpy restatement; the augmented KPM
     step y = 2a(H - bI)x - y with <y,y>, <x,y>, <x,x> (w = 16, complex) is bit-identical
