@@ -53,7 +53,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=400, help="grid edge of the 3-D 7-point stencil")
+    p.add_argument("--n", "--edge", dest="n", type=int, default=400, help="grid edge of the 3-D 7-point stencil")
     p.add_argument("--width", type=int, default=8)
     p.add_argument("--chunk", type=int, default=32)
     p.add_argument("--sigma", type=int, default=256)
@@ -474,8 +474,11 @@ def spawn_ranks(args) -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
+    # torch.distributed.run's parser takes "--n" for an abbreviation of its own options: pass
+    # the grid edge under its unambiguous name
+    fwd = ["--edge" if a == "--n" else ("--edge=" + a[4:] if a.startswith("--n=") else a) for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + fwd
     return subprocess.run(cmd).returncode
 
 
