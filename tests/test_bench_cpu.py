@@ -43,3 +43,26 @@ def test_multi_gpu_request_needs_the_gpus():
     r = _run("--gpus", "2", "--steps", "1", "--warmup", "1", timeout=300)
     assert r.returncode != 0
     assert "needs 2 visible GPUs" in r.stderr
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """The driver launches the reference arm like its own (torchrun, N ranks): rank 0 alone
+    runs and prints; the other ranks exit 0 without output."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libsellkit.so")):
+        pytest.skip("reference library not built")
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    e = dict(os.environ, OMP_NUM_THREADS="2")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE"):
+        e.pop(k, None)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--edge", "24", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=e)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["value"] > 0
