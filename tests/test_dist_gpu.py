@@ -112,6 +112,34 @@ def test_dist_fused_vs_serial(sk, orc, k, mode):
     assert np.all(np.abs(dots - do) <= 1e-12 * (1 + np.abs(do)))
 
 
+@pytest.mark.parametrize("k", [2, 3])
+def test_dist_wide_rows(sk, orc, k):
+    """512-B RHS rows (w = 64) through the distributed path: the remote-part sweep takes the
+    row-mapped wide-row kernel; every flag against the serial fused SpMV (1e-12)."""
+    n, w = 12, 64
+    N = n ** 3
+    rp, c, v = stencil_crs(7, n)
+    ctx = dist.DistContext(sk, sk.crs(rp, c, v), k, 32, 64, record=False)
+    xv, y0, z0 = hash_block(N, w, 4), hash_block(N, w, 5), hash_block(N, w, 6)
+    dx, dy, dz = ctx.vec(w), ctx.vec(w), ctx.vec(w)
+    for arr, dv in [(xv, dx), (y0, dy), (z0, dz)]:
+        ctx.scatter(sk.densemat_from(arr), dv)
+    flags = (sellkit.AXPBY | sellkit.SHIFT | sellkit.DOT_YY | sellkit.DOT_XY | sellkit.DOT_XX |
+             sellkit.CHAIN_AXPBY)
+    dots = np.zeros(3 * w)
+    ctx.spmv(dy, dx, flags=flags, alpha=0.5, beta=-1.0, gamma=0.25, delta=1.0, eta=0.3, z=dz, dot=dots,
+             mode=sellkit.TASK_OVERLAP)
+    yg, zg = sk.densemat(N, w), sk.densemat(N, w)
+    ctx.gather(dy, yg)
+    ctx.gather(dz, zg)
+    A = orc.build(rp, c, v, 1, 1)
+    yo, zo, do = orc.spmv(A, xv, y0, z0, flags, alpha=0.5, beta=-1.0, gamma=0.25, delta=1.0, eta=0.3)
+    rel = lambda a, b: np.max(np.abs(a - b) / (1 + np.abs(b)))  # noqa: E731
+    assert rel(yg.copy_out(), yo) < 1e-12
+    assert rel(zg.copy_out(), zo) < 1e-12
+    assert np.all(np.abs(dots - do) <= 1e-12 * (1 + np.abs(do)))
+
+
 def test_nocomm_is_local_only(sk, orc):
     """spmv_nocomm drops the remote columns (partition.hpp:554-600)."""
     n, w, k = 8, 2, 4
