@@ -75,6 +75,7 @@ struct KArgs {
                              // concurrent halo pack on the communication stream)
     int* tile_counter;       // rows kernels without dots: tiles handed out by an atomic counter
                              // (zeroed before the launch) instead of a static round robin
+    int grp_end;             // rows kernel (set at launch): min(nrows_padded, 32 rg1)
 #if SK_CHECK
     lidx xrows;              // checked build: rows of x (gather bound)
     gidx slots;              // checked build: stored slots of the matrix
@@ -1147,7 +1148,9 @@ __global__ void __launch_bounds__(kTmaThreads, rows_minb<T, W, DOTS>())
         // address IMAD.WIDEs
         const int rg0 = int(a.rg0);
         const int nt = int(ntiles);
-        const int grp_end = int(min(gidx(a.nrows_padded), a.rg1 * 32));  // warps at/after: idle
+        // (the epilogue-free kernels read grp_end from the parameter bank where they use it:
+        // kept in a register it was the one value they spilled, reloaded every tile)
+        const int grp_end = PLAIN ? 0 : int(min(gidx(a.nrows_padded), a.rg1 * 32));  // warps at/after: idle
         const int row_end = int(min(gidx(a.nrows), a.rg1 * 32));          // rows stored
         // (compile-time bound: one pass for the dots variant, whose register budget
         // has no room for the pass loop -- measured 30 % slower on C3 C64)
@@ -1169,7 +1172,7 @@ __global__ void __launch_bounds__(kTmaThreads, rows_minb<T, W, DOTS>())
             // per-tile work (barrier, header, release) is shared by all of them
             for (int pass = 0; pass < passes; ++pass) {
             const int wrow0 = (pass * kNCW + warp) * WR;  // this warp's first row of the pass
-            if (wrow0 >= rows_per_tile || tile_row0 + wrow0 >= grp_end) break;  // warp-uniform
+            if (wrow0 >= rows_per_tile || tile_row0 + wrow0 >= (PLAIN ? a.grp_end : grp_end)) break;  // warp-uniform
             const int rr = wrow0 + rl;
             const int row = tile_row0 + rr;
             const int cq = rr / C;
@@ -1602,6 +1605,7 @@ template <class T, int C, int W, bool DOTS, bool PLAIN, bool MAPPED = false,
 LaunchShape launch_tma_rows(const KArgs<T>& a_in, int rgt, DeviceRuntime& rt, cudaStream_t st) {
     KArgs<T> a = a_in;
     if (!DYN) a.tile_counter = nullptr;
+    a.grp_end = int(std::min<gidx>(gidx(a.nrows_padded), a.rg1 * 32));
     constexpr int U = rows_unroll<T, W, DOTS>();
     auto kern = spmv_tma_rows_kernel<T, C, W, U, DOTS, PLAIN, MAPPED, DYN>;
     constexpr std::size_t smem = rows_smem_bytes<T, W, DOTS>();
