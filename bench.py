@@ -456,7 +456,8 @@ def run_ours(args, rank, world, local_rank):
         build["spmv_units_update_values"] = build["update_values_ms"] / ms_per_step
         build["what"] = ("median wall time of 3 synchronous sellkit_mat_build calls (CRS in HBM -> SELL-C-sigma: "
                          "sigma-sort, permutation, chunk lengths/offsets, fill) and sellkit_mat_update_values, over "
-                         "ms_per_step")
+                         "ms_per_step; the 2nd and 3rd build reuse the freed matrix's device memory through the "
+                         "library's buffer cache (build_ms_each[0]: with the driver allocations)")
         line["construction"] = build
     print(json.dumps(line), flush=True)
 

@@ -326,12 +326,11 @@ void exclusive_scan_i64(const gidx* in, gidx* out, gidx n, DeviceRuntime& rt) {
 
 void crs_validate_impl(const Crs& a, bool check_sorted) {
     auto& rt = runtime(a.device);
-    DeviceBuffer flag(sizeof(int), a.device);
-    CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), rt.stream));
+    int* flag = rt.flag();
     crs_validate_kernel<<<blocks_for(std::max<gidx>(a.nrows, 1)), kThreads, 0, rt.stream>>>(
-        a.rowptr.as<gidx>(), a.col.as<gidx>(), a.nrows, a.ncols, check_sorted ? 1 : 0, flag.as<int>());
+        a.rowptr.as<gidx>(), a.col.as<gidx>(), a.nrows, a.ncols, check_sorted ? 1 : 0, flag);
     CK(cudaGetLastError());
-    const int e = read_flag(flag, rt);
+    const int e = rt.read_flag();
     SK_REQUIRE(!(e & kErrRowptrStart), errc::invalid_arg, "rowptr must start at 0");
     SK_REQUIRE(!(e & kErrRowptrOrder), errc::invalid_arg, "rowptr must be non-decreasing");
     SK_REQUIRE(!(e & kErrColRange), errc::invalid_arg, "column index out of range");
@@ -429,7 +428,7 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
     m->nnz = a.nnz;
 
 
-    m->row_perm_inv = DeviceBuffer(std::size_t(n) * sizeof(lidx), a.device);
+    m->row_perm_inv = DeviceBuffer::cached(std::size_t(n) * sizeof(lidx), a.device);
     lidx* pinv = m->row_perm_inv.as<lidx>();
     if (opt.imposed_order) {
         CK(cudaMemcpyAsync(pinv, opt.imposed_order, std::size_t(n) * sizeof(lidx), cudaMemcpyDefault, rt.stream));
@@ -442,9 +441,9 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
             scope_sort_kernel<<<unsigned(nscopes), kSortThreads, std::size_t(scope) * sizeof(lidx), rt.stream>>>(
                 a.rowptr.as<gidx>(), n, scope, pinv);
         } else {
-            DeviceBuffer lens(std::size_t(n) * sizeof(lidx), a.device);
+            auto lens = DeviceBuffer::pooled(std::size_t(n) * sizeof(lidx), a.device);
             row_lengths_kernel<<<blocks_for(n), kThreads, 0, rt.stream>>>(a.rowptr.as<gidx>(), n, lens.as<lidx>());
-            DeviceBuffer mx(sizeof(int), a.device);
+            auto mx = DeviceBuffer::pooled(sizeof(int), a.device);
             CK(cudaMemsetAsync(mx.get(), 0, sizeof(int), rt.stream));
             max_kernel<<<std::min(blocks_for(n), rt.num_sms * 4), kThreads, 0, rt.stream>>>(lens.as<lidx>(), n,
                                                                                        mx.as<int>());
@@ -454,8 +453,9 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
             const gidx nscopes = (gidx(n) + scope - 1) / scope;
             int scope_bits = 0;
             while ((gidx(1) << scope_bits) < nscopes) ++scope_bits;
-            DeviceBuffer keys(std::size_t(n) * 8, a.device), keys2(std::size_t(n) * 8, a.device);
-            DeviceBuffer idx(std::size_t(n) * 4, a.device);
+            auto keys = DeviceBuffer::pooled(std::size_t(n) * 8, a.device);
+            auto keys2 = DeviceBuffer::pooled(std::size_t(n) * 8, a.device);
+            auto idx = DeviceBuffer::pooled(std::size_t(n) * 4, a.device);
             scope_keys_kernel<<<blocks_for(n), kThreads, 0, rt.stream>>>(lens.as<lidx>(), n, scope, maxlen, len_bits,
                                                                           keys.as<unsigned long long>(), idx.as<lidx>());
             std::size_t tmp_bytes = 0;
@@ -463,7 +463,7 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.as<unsigned long long>(),
                                                keys2.as<unsigned long long>(), idx.as<lidx>(), pinv, n, 0, end_bit,
                                                rt.stream));
-            DeviceBuffer tmp(std::max<std::size_t>(tmp_bytes, 1), a.device);
+            auto tmp = DeviceBuffer::pooled(std::max<std::size_t>(tmp_bytes, 1), a.device);
             CK(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.as<unsigned long long>(),
                                                keys2.as<unsigned long long>(), idx.as<lidx>(), pinv, n, 0, end_bit,
                                                rt.stream));
@@ -476,13 +476,13 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
     m->nchunks = nchunks;
     SK_REQUIRE(nchunks * C < (gidx(1) << 31), errc::overflow, "padded row count exceeds the 32-bit range");
     m->nrows_padded = lidx(nchunks * C);
-    m->row_perm = DeviceBuffer(std::size_t(n) * sizeof(lidx), a.device);
-    m->rowlen = DeviceBuffer(std::size_t(m->nrows_padded) * sizeof(lidx), a.device);
-    m->chunk_len = DeviceBuffer(std::size_t(nchunks) * sizeof(lidx), a.device);
-    m->chunk_offset = DeviceBuffer(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
+    m->row_perm = DeviceBuffer::cached(std::size_t(n) * sizeof(lidx), a.device);
+    m->rowlen = DeviceBuffer::cached(std::size_t(m->nrows_padded) * sizeof(lidx), a.device);
+    m->chunk_len = DeviceBuffer::cached(std::size_t(nchunks) * sizeof(lidx), a.device);
+    m->chunk_offset = DeviceBuffer::cached(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
     {
-        DeviceBuffer sizes(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
-        DeviceBuffer out(2 * sizeof(gidx), a.device);  // {max chunk length, slots}
+        auto sizes = DeviceBuffer::pooled(std::size_t(nchunks + 1) * sizeof(gidx), a.device);
+        auto out = DeviceBuffer::pooled(2 * sizeof(gidx), a.device);  // {max chunk length, slots}
         CK(cudaMemsetAsync(out.get(), 0, sizeof(gidx), rt.stream));
         const bool fused = 32 % C == 0;
         (fused ? perm_kernel<true> : perm_kernel<false>)<<<blocks_for(gidx(m->nrows_padded) + 1), kThreads, 0,
@@ -498,7 +498,7 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
         std::size_t tmp_bytes = 0;
         CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, sizes.as<gidx>(), m->chunk_offset.as<gidx>(),
                                          nchunks + 1, rt.stream));
-        DeviceBuffer tmp(std::max<std::size_t>(tmp_bytes, 1), rt.device);
+        auto tmp = DeviceBuffer::pooled(std::max<std::size_t>(tmp_bytes, 1), rt.device);
         CK(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, sizes.as<gidx>(), m->chunk_offset.as<gidx>(),
                                          nchunks + 1, rt.stream));
         CK(cudaMemcpyAsync(out.as<gidx>() + 1, m->chunk_offset.as<gidx>() + nchunks, sizeof(gidx),
@@ -512,19 +512,18 @@ std::unique_ptr<SellMat> sell_build(const Crs& a, lidx C, lidx sigma, const Buil
     m->beta = m->slots > 0 ? double(m->nnz) / double(m->slots) : 1.0;
 
     const std::size_t es = value_bytes(a.dt);
-    m->val = DeviceBuffer(std::max<std::size_t>(std::size_t(m->slots) * es, 16), a.device);
-    m->col = DeviceBuffer(std::max<std::size_t>(std::size_t(m->slots) * sizeof(lidx), 16), a.device);
-    DeviceBuffer flag(sizeof(int), a.device);
-    CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), rt.stream));
+    m->val = DeviceBuffer::cached(std::max<std::size_t>(std::size_t(m->slots) * es, 16), a.device);
+    m->col = DeviceBuffer::cached(std::max<std::size_t>(std::size_t(m->slots) * sizeof(lidx), 16), a.device);
+    int* flag = rt.flag();
     visit_dt(a.dt, [&]<class T>() {
         fill_kernel<T><<<blocks_for(m->nrows_padded), kThreads, 0, rt.stream>>>(
             a.rowptr.as<gidx>(), a.col.as<gidx>(), a.val.as<T>(), pinv, m->row_perm.as<lidx>(), m->rowlen.as<lidx>(),
             m->chunk_len.as<lidx>(), m->chunk_offset.as<gidx>(), n, m->nrows_padded, C, a.ncols,
-            m->cols_permuted ? 1 : 0, m->val.as<T>(), m->col.as<lidx>(), flag.as<int>());
+            m->cols_permuted ? 1 : 0, m->val.as<T>(), m->col.as<lidx>(), flag);
         return 0;
     });
     CK(cudaGetLastError());
-    const int e = read_flag(flag, rt);
+    const int e = rt.read_flag();
     SK_REQUIRE(!(e & kErrColRange), errc::invalid_arg, "column index out of range");
     return m;
 }
@@ -535,16 +534,15 @@ void sell_update_values(SellMat& m, const Crs& a) {
     SK_REQUIRE(a.dt == m.dt, errc::invalid_arg, "datatype mismatch between matrix and CRS data");
     DeviceGuard g(m.device);
     auto& rt = runtime(m.device);
-    DeviceBuffer flag(sizeof(int), m.device);
-    CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), rt.stream));
+    int* flag = rt.flag();
     visit_dt(m.dt, [&]<class T>() {
         update_values_kernel<T><<<blocks_for(m.nrows), kThreads, 0, rt.stream>>>(
             a.rowptr.as<gidx>(), a.val.as<T>(), m.row_perm.as<lidx>(), m.rowlen.as<lidx>(), m.chunk_offset.as<gidx>(),
-            m.nrows, m.C, m.val.as<T>(), flag.as<int>());
+            m.nrows, m.C, m.val.as<T>(), flag);
         return 0;
     });
     CK(cudaGetLastError());
-    const int e = read_flag(flag, rt);
+    const int e = rt.read_flag();
     SK_REQUIRE(!(e & kErrPattern), errc::pattern_mismatch, "row length differs from the stored pattern");
 }
 

@@ -146,6 +146,14 @@ public:
         swap(t);
         return *this;
     }
+    // Stream-ordered allocation from the device's library pool (SELL storage and build
+    // temporaries): freed memory stays in the pool, so a rebuild or a value refresh makes
+    // no driver allocation.  Not for memory that is exported through CUDA IPC.
+    static DeviceBuffer pooled(std::size_t bytes, int device);
+    // cudaMalloc'ed, but returned to a per-device cache on destruction and reused by the next
+    // request of the same size (SELL storage: a rebuild or a second matrix of the same shape
+    // makes no driver allocation; the cache is bounded, DeviceRuntime::cache_*).
+    static DeviceBuffer cached(std::size_t bytes, int device);
     void* get() const { return ptr_; }
     template <class T>
     T* as() const { return static_cast<T*>(ptr_); }
@@ -155,12 +163,16 @@ public:
         std::swap(ptr_, o.ptr_);
         std::swap(bytes_, o.bytes_);
         std::swap(device_, o.device_);
+        std::swap(pooled_, o.pooled_);
+        std::swap(cached_, o.cached_);
     }
 
 private:
     void* ptr_ = nullptr;
     std::size_t bytes_ = 0;
     int device_ = 0;
+    bool pooled_ = false;
+    bool cached_ = false;
 };
 
 // ------------------------------------------------------------------ runtime --
@@ -187,6 +199,18 @@ struct DeviceRuntime {
 
     void* scratch_bytes(std::size_t n);
     void* pinned_bytes_at_least(std::size_t n);
+    cudaMemPool_t pool = nullptr;  // DeviceBuffer::pooled (created on first use, keeps its memory)
+    // DeviceBuffer::cached: freed (pointer, bytes), most recent last, at most cache_cap bytes
+    std::vector<std::pair<void*, std::size_t>> cache;
+    std::size_t cache_bytes = 0, cache_cap = 0;
+    void* cache_take(std::size_t bytes);
+    void cache_put(void* p, std::size_t bytes);
+    cudaMemPool_t mem_pool();
+    // one device word + its pinned host mirror for error flags / small readbacks
+    int* flag_dev = nullptr;
+    int* flag_host = nullptr;
+    int* flag();                     // zeroed on the stream, ready for a kernel to OR into
+    int read_flag();                 // synchronises the stream
 };
 
 DeviceRuntime& runtime(int device);

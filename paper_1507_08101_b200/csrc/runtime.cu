@@ -41,14 +41,111 @@ DeviceBuffer::DeviceBuffer(std::size_t bytes, int device) : bytes_(bytes), devic
     CK(cudaMalloc(&ptr_, bytes));
 }
 
+DeviceBuffer DeviceBuffer::pooled(std::size_t bytes, int device) {
+    DeviceBuffer b;
+    b.bytes_ = bytes;
+    b.device_ = device;
+    if (bytes == 0) return b;
+    DeviceGuard g(device);
+    auto& rt = runtime(device);
+    CK(cudaMallocFromPoolAsync(&b.ptr_, bytes, rt.mem_pool(), rt.stream));
+    b.pooled_ = true;
+    return b;
+}
+
+DeviceBuffer DeviceBuffer::cached(std::size_t bytes, int device) {
+    DeviceBuffer b;
+    b.bytes_ = bytes;
+    b.device_ = device;
+    if (bytes == 0) return b;
+    DeviceGuard g(device);
+    b.ptr_ = runtime(device).cache_take(bytes);
+    if (!b.ptr_) CK(cudaMalloc(&b.ptr_, bytes));
+    b.cached_ = true;
+    return b;
+}
+
+void* DeviceRuntime::cache_take(std::size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (std::size_t i = cache.size(); i-- > 0;) {
+        if (cache[i].second == bytes) {
+            void* p = cache[i].first;
+            cache_bytes -= bytes;
+            cache.erase(cache.begin() + std::ptrdiff_t(i));
+            return p;
+        }
+    }
+    return nullptr;
+}
+
+void DeviceRuntime::cache_put(void* p, std::size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache_cap == 0) {
+        std::size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        cache_cap = std::max<std::size_t>(tot / 8, std::size_t(1) << 30);  // 22 GB on a B200
+    }
+    if (bytes > cache_cap) {
+        cudaFree(p);
+        return;
+    }
+    while (!cache.empty() && cache_bytes + bytes > cache_cap) {  // drop the oldest
+        cudaFree(cache.front().first);
+        cache_bytes -= cache.front().second;
+        cache.erase(cache.begin());
+    }
+    cache.emplace_back(p, bytes);
+    cache_bytes += bytes;
+}
+
 DeviceBuffer::~DeviceBuffer() {
     if (ptr_) {
         int prev = 0;
         cudaGetDevice(&prev);
         if (prev != device_) cudaSetDevice(device_);
-        cudaFree(ptr_);
+        if (cached_) {
+            cudaDeviceSynchronize();  // what cudaFree would order: nothing in flight still uses it
+            runtime(device_).cache_put(ptr_, bytes_);
+        } else if (pooled_) {
+            // the same ordering cudaFree gives: nothing in flight on any stream of the device
+            // may still use the memory when the pool hands it out again
+            cudaDeviceSynchronize();
+            cudaFreeAsync(ptr_, runtime(device_).stream);
+        } else {
+            cudaFree(ptr_);
+        }
         if (prev != device_) cudaSetDevice(prev);
     }
+}
+
+cudaMemPool_t DeviceRuntime::mem_pool() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pool) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        CK(cudaMemPoolCreate(&pool, &props));
+        std::uint64_t keep = ~std::uint64_t(0);  // never trim at synchronisation points
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
+    return pool;
+}
+
+int* DeviceRuntime::flag() {
+    if (!flag_dev) {
+        DeviceGuard g(device);
+        CK(cudaMalloc(reinterpret_cast<void**>(&flag_dev), 256));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&flag_host), 256));
+    }
+    CK(cudaMemsetAsync(flag_dev, 0, sizeof(int), stream));
+    return flag_dev;
+}
+
+int DeviceRuntime::read_flag() {
+    CK(cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    return *flag_host;
 }
 
 void* DeviceRuntime::scratch_bytes(std::size_t n) {
@@ -121,6 +218,15 @@ DeviceRuntime& runtime(int device) {
     int l2 = 0;
     CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
     rt->l2_bytes = std::size_t(l2);
+    // the build-temporary pool and the flag word exist from the first call on, and the pool
+    // holds 64 MB from the start, so a first matrix build does not pay their creation
+    {
+        void* p = nullptr;
+        CK(cudaMallocFromPoolAsync(&p, std::size_t(64) << 20, rt->mem_pool(), rt->stream));
+        CK(cudaFreeAsync(p, rt->stream));
+        rt->flag();
+        CK(cudaStreamSynchronize(rt->stream));
+    }
     reg[device] = rt;
     return *rt;
 }
