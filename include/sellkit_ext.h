@@ -28,6 +28,10 @@ sellkit_error sellkit_ext_set_sync(int sync);
 sellkit_error sellkit_ext_synchronize(void);
 sellkit_error sellkit_ext_stream(void** stream);
 sellkit_error sellkit_ext_device_info(int* device, int* num_sms, size_t* l2_bytes);
+/* Device memory the library keeps for reuse -- freed SELL storage (up to 1/8 of each
+ * device's memory, reused by the next matrix of the same size) and the build-temporary
+ * pool -- is returned to the driver on every device the library has used. */
+sellkit_error sellkit_ext_release_cached(void);
 
 /* ------------------------------------------------------------ CRS input -- */
 /* Same as sellkit_crs_create with device (or any UVA) pointers. */

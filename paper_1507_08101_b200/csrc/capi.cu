@@ -644,6 +644,10 @@ sellkit_error sellkit_ext_synchronize(void) {
     return guarded([&] { CK(cudaStreamSynchronize(sk::runtime(sk::current_device()).stream)); });
 }
 
+sellkit_error sellkit_ext_release_cached(void) {
+    return guarded([&] { sk::release_cached_all(); });
+}
+
 sellkit_error sellkit_ext_stream(void** stream) {
     return guarded([&] {
         require(stream != nullptr, "null output");

@@ -214,6 +214,7 @@ struct DeviceRuntime {
 };
 
 DeviceRuntime& runtime(int device);
+void release_cached_all();  // DeviceRuntime caches and pools of every device -> driver
 int current_device();
 void set_last_error(const char* msg);  // per-thread message of the last failed C-ABI call
 const char* last_error_message();

@@ -231,6 +231,23 @@ DeviceRuntime& runtime(int device) {
     return *rt;
 }
 
+void release_cached_all() {
+    std::vector<DeviceRuntime*> rts;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        for (auto& kv : registry()) rts.push_back(kv.second);
+    }
+    for (auto* rt : rts) {
+        DeviceGuard g(rt->device);
+        CK(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(rt->mu);
+        for (auto& e : rt->cache) cudaFree(e.first);
+        rt->cache.clear();
+        rt->cache_bytes = 0;
+        if (rt->pool) CK(cudaMemPoolTrimTo(rt->pool, 0));
+    }
+}
+
 namespace {
 thread_local std::string t_last_error;
 }

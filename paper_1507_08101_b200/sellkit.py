@@ -146,6 +146,7 @@ _EXT = [
     ("sellkit_ext_last_error", C.c_char_p, []),
     ("sellkit_ext_set_sync", err_t, [C.c_int]),
     ("sellkit_ext_synchronize", err_t, []),
+    ("sellkit_ext_release_cached", err_t, []),
     ("sellkit_ext_stream", err_t, [C.POINTER(vp)]),
     ("sellkit_ext_device_info", err_t, [C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_size_t)]),
     ("sellkit_ext_crs_create_device", err_t, [C.c_int, gidx, gidx, vp, vp, vp, C.POINTER(vp)]),

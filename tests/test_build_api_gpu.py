@@ -182,3 +182,19 @@ def test_sigma_permutation_stable_descending(sk, orc, sigma, maxlen):
         R = orc.build(rp, col, val, C_, sigma).layout()
         for key in LAYOUT:
             assert np.array_equal(L[key], R[key]), (C_, key)
+
+
+def test_buffer_cache_reuse_and_release(sk):
+    """Freed SELL storage is reused by the next build of the same size (layout unchanged) and
+    returned to the driver by sellkit_ext_release_cached; builds after the release still work."""
+    rp, col, val = _irregular(seed=9, n=900)
+    crs = sk.crs(rp, col, val)
+    first = crs.build(32, 64).export()
+    for _ in range(2):
+        again = crs.build(32, 64).export()  # the previous Mat was freed into the cache
+        for key in LAYOUT:
+            assert np.array_equal(first[key], again[key]), key
+    sk.call("sellkit_ext_release_cached")
+    after = crs.build(32, 64).export()
+    for key in LAYOUT:
+        assert np.array_equal(first[key], after[key]), key
